@@ -1,0 +1,131 @@
+/*
+ * chfsi_b200.h -- C ABI of libchfsi_b200.so, the B200 (sm_100a) ChFSI hot path.
+ *
+ * The reference (arxiv 1305.5120 Python package `chfsi`, /root/reference/pkg)
+ * has no native FFI: its hot path calls numpy/scipy/numba. Each entry point
+ * below replaces one of those calls; the comment names the reference
+ * interface it stands in for (file:line under pkg/src/chfsi/). A ctypes
+ * binding (paper_1305_5120_b200/_native.py) is the only
+ * caller.
+ *
+ * Conventions
+ *   - complex128 matrices are interleaved (re, im) doubles, COLUMN-MAJOR with
+ *     a leading dimension `ld*` counted in complex elements: numpy F-order.
+ *   - pointers named d_* are DEVICE pointers on the handle's device; h_* are
+ *     host pointers. Calls that return host data synchronise the stream.
+ *   - every function returns 0 on success or a negative status; the message
+ *     is in chfsi_last_error() (thread-local). Status codes:
+ *        -1 CHFSI_ERR_ARG       contract violation
+ *        -2 CHFSI_ERR_CUDA      CUDA runtime error
+ *        -3 CHFSI_ERR_CUSOLVER  cuSOLVER error
+ *        -4 CHFSI_ERR_NOT_PD    Cholesky pivot failed (info = 1-based pivot)
+ *        -5 CHFSI_ERR_RANK      rank collapse (bad column, 0-based)
+ *        -6 CHFSI_ERR_NOMEM     device allocation failed
+ *   - op codes: 0 = N (as is), 1 = C (conjugate transpose).
+ */
+#ifndef CHFSI_B200_H
+#define CHFSI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHFSI_ABI_VERSION 1
+
+typedef struct chfsi_handle_s* chfsi_handle_t;
+
+int chfsi_abi_version(void);
+const char* chfsi_last_error(void);
+
+/* Context: cuSOLVER handle, scratch arenas, stream binding (one per device). */
+int chfsi_create(int device, void* stream, chfsi_handle_t* out);
+int chfsi_destroy(chfsi_handle_t h);
+int chfsi_set_stream(chfsi_handle_t h, void* stream);
+int chfsi_synchronize(chfsi_handle_t h);
+/* kernels (and cuSOLVER calls) this handle has launched; reset with reset=1 */
+long long chfsi_launch_count(chfsi_handle_t h, int reset);
+
+/* C = alpha op(A) op(B) + beta C on the FP64 tensor pipe (DMMA).
+ * Replaces linalg.py:198-251 `gemm` (numpy zgemm through OpenBLAS). */
+int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_t k,
+                double alpha_re, double alpha_im, const void* d_A, int64_t lda,
+                const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
+                int64_t ldc);
+
+/* Scaled degree-m Chebyshev filter p_m(H) Y, core.py:263-284 `_filter_raw`.
+ * d_Y (n x k) is clobbered; the result is in d_W when *h_result_in_w == 1,
+ * else in d_Y. Exactly `degree` fused GEMM launches (H streamed once each). */
+int chfsi_filter(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a, double b,
+                 double lam_ref, const void* d_H, int64_t ldh, void* d_Y, int64_t ldy,
+                 void* d_W, int64_t ldw, int* h_result_in_w);
+
+/* One fused degree step C = alpha H Y1 + beta Y1 + gamma Y0 (Y0 may be NULL and may
+ * alias C); the unit the filter roofline is measured on (core.py:280-281). */
+int chfsi_filter_step(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
+                      const void* d_Y1, int64_t ld1, double alpha, double beta,
+                      const void* d_Y0, int64_t ld0, double gamma, void* d_C, int64_t ldc);
+
+/* k-step Lanczos with full reorthogonalisation, core.py:202-256
+ * `lanczos_upper_bound`. d_v0 = normalised start vector (drawn by the caller
+ * from the reference's Generator stream). Returns alphas/betas (length >= k),
+ * the steps taken and b = lambda_max(T) + beta_last + 4 j eps max|lambda(T)|. */
+int chfsi_lanczos_bound(chfsi_handle_t h, int64_t n, int k, const void* d_H, int64_t ldh,
+                        const void* d_v0, double* h_alphas, double* h_betas, int* h_steps,
+                        double* h_bound);
+
+/* core.py:365-382 `_qr_against_locked` (+ linalg.py:273-289 rank test):
+ * F <- F - L (L^H F) twice (CGS2), then Q = CholQR2(F) (shifted CholQR3 if the
+ * first Cholesky breaks down). d_T is an n x k work block. Returns
+ * CHFSI_ERR_RANK with *h_bad_col = first column whose |R_jj| < rank_tol*||F||_F.
+ * *h_fro = ||F||_F after projection. */
+int chfsi_orthonormalize(chfsi_handle_t h, int64_t n, int64_t k, void* d_F, int64_t ldf,
+                         const void* d_L, int64_t ldl, int64_t nl, void* d_T, int64_t ldt,
+                         void* d_Q, int64_t ldq, double rank_tol, int64_t* h_bad_col,
+                         double* h_fro);
+
+/* core.py:318-330 `_rr_raw`: HQ = H Q, G = Q^H HQ, G <- (G+G^H)/2, (w, W) = eig(G)
+ * (cuSOLVER zheevd, ascending), Z = Q W, HZ = HQ W. Ritz values to h_w (k). */
+int chfsi_rayleigh_ritz(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
+                        const void* d_Q, int64_t ldq, void* d_HQ, int64_t ldhq, void* d_Z,
+                        int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w);
+
+/* r_j = ||HY_j - lam_j Y_j||_2, core.py:347-358 `residuals` and core.py:477. */
+int chfsi_residual_norms(chfsi_handle_t h, int64_t n, int64_t k, const void* d_HY, int64_t ldhy,
+                         const void* d_Y, int64_t ldy, const double* h_lam, double* h_res);
+
+/* linalg.py:104-121 HermitianDenseMatrix: h_out[0] = ||A||_F, h_out[1] = ||A - A^H||_F. */
+int chfsi_hermitian_norms(chfsi_handle_t h, int64_t n, const void* d_A, int64_t lda,
+                          double* h_out);
+/* A <- (A + A^H)/2 with a real diagonal (linalg.py:114-115). */
+int chfsi_hermitize(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda);
+
+/* linalg.py:254-270 `cholesky_factor`: in-place lower Cholesky (cuSOLVER zpotrf),
+ * upper triangle zeroed and diagonal made real. *h_info = failing pivot (1-based) or 0. */
+int chfsi_cholesky(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, int* h_info);
+
+/* X = L^-1 for lower-triangular L (blocked recursive inverse on the DMMA GEMM);
+ * building block of linalg.py:326-366 `triangular_solve` / `trmm_adjoint`. */
+int chfsi_trtri_lower(chfsi_handle_t h, int64_t n, const void* d_L, int64_t ldl, void* d_X,
+                      int64_t ldx);
+
+/* Full Hermitian eigendecomposition in place (cuSOLVER zheevd), ascending.
+ * Stands in for linalg.py:292-323 `oracle_eig` / `_jacobi_raw` on the device. */
+int chfsi_heevd(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, double* h_w);
+
+/* Y = alpha X + beta Y on an n x k block (X may be NULL). */
+int chfsi_axpby(chfsi_handle_t h, int64_t n, int64_t k, double alpha_re, double alpha_im,
+                const void* d_X, int64_t ldx, double beta_re, double beta_im, void* d_Y,
+                int64_t ldy);
+
+/* Microbenchmarks that give the roofline denominators on the box:
+ * FP64 tensor-pipe (DMMA) and FP64 FMA-pipe (DFMA) peak, TFLOP/s. */
+int chfsi_peak_dmma(int device, int iters, double* h_tflops);
+int chfsi_peak_dfma(int device, int iters, double* h_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHFSI_B200_H */

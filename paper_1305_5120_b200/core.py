@@ -1,0 +1,570 @@
+"""ChFSI solver on the B200, behind the reference's chfsi.core API
+(reference pkg/src/chfsi/core.py:59-569).
+
+The outer loop (locking, interval updates, RNG order, report, errors) is
+restated here line for line from core.py:385-546 so traces stay comparable
+with the reference; every n x n x k product, the QR, the Rayleigh-Ritz
+projection and the residual norms run as CUDA kernels in libchfsi_b200.so on
+device-resident blocks. Per outer iteration the host sees only the k Ritz
+values, k residuals and (for the rank test) k diagonal entries.
+
+Buffers (all column-major complex128, n x (nev+buffer)): two filter blocks,
+HQ, Z, HZ, plus the locked block (n x nev); H stays resident.
+"""
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .errors import ContractViolation, FilterDegenerate, NotConverged, RankDeficient
+from .linalg import (
+    HermitianDenseMatrix,
+    LowerTriangularFactor,
+    VectorBlock,
+    _count_products,
+    cholesky_factor,
+    default_device,
+    engine,
+    solve_triangular_device,
+    to_block,
+)
+
+__all__ = [
+    "FilterSpec", "SolverConfig", "SolveReport", "IterationStat", "reduce_to_standard",
+    "back_transform", "lanczos_upper_bound", "chebyshev_filter", "rayleigh_ritz",
+    "residuals", "chfsi_solve", "solve_generalized",
+]
+
+
+# ----------------------------------------------------------------------
+# configuration and reporting types (core.py:59-165)
+
+
+@dataclass(frozen=True)
+class FilterSpec:
+    """Chebyshev filter parameters (core.py:59-79)."""
+
+    degree: int
+    a: float
+    b: float
+    lam_ref: float
+
+    def __post_init__(self):
+        if self.degree < 1:
+            raise ContractViolation(f"filter degree must be >= 1, got {self.degree}")
+        if not self.a < self.b:
+            raise ContractViolation(f"filter interval requires a < b, got a={self.a}, b={self.b}")
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Solver knobs (core.py:82-115). ``interval`` is a B200-build extension:
+    "reference" (default) puts the filter's lower edge at Ritz value nev+1
+    exactly like core.py:507-509; "block_top" puts it at the largest Ritz value
+    of the search block (ChASE-style, SURVEY.md section 7 ii), opt-in only."""
+
+    nev: int
+    tol: float = 1e-10
+    max_outer_iters: int = 30
+    degree: int = 20
+    lanczos_steps: int = 10
+    buffer: int | None = None
+    interval: str = "reference"
+
+    def __post_init__(self):
+        if self.nev < 1:
+            raise ContractViolation(f"nev must be >= 1, got {self.nev}")
+        if not self.tol > 0:
+            raise ContractViolation(f"tol must be > 0, got {self.tol}")
+        if self.max_outer_iters < 1:
+            raise ContractViolation("max_outer_iters must be >= 1")
+        if self.degree < 1:
+            raise ContractViolation("degree must be >= 1")
+        if self.lanczos_steps < 2:
+            raise ContractViolation("lanczos_steps must be >= 2")
+        if self.buffer is not None and self.buffer < 1:
+            raise ContractViolation("buffer must be >= 1 when given")
+        if self.interval not in ("reference", "block_top"):
+            raise ContractViolation(f"unknown interval placement {self.interval!r}")
+
+    @property
+    def buffer_cols(self):
+        if self.buffer is not None:
+            return self.buffer
+        return max(1, math.ceil(0.1 * self.nev))
+
+
+def _as_config(config):
+    """Accept our SolverConfig or any object with the reference's fields
+    (e.g. the reference's own chfsi.core.SolverConfig, core.py:402-403)."""
+    if isinstance(config, SolverConfig):
+        return config
+    fields = ("nev", "tol", "max_outer_iters", "degree", "lanczos_steps", "buffer")
+    if all(hasattr(config, f) for f in fields):
+        return SolverConfig(**{f: getattr(config, f) for f in fields})
+    raise ContractViolation("config must be a SolverConfig")
+
+
+@dataclass
+class IterationStat:
+    """Per-outer-iteration statistics (core.py:118-131)."""
+
+    iteration: int
+    filtered_cols: int
+    converged: int
+    max_resid: float
+    min_resid: float
+    matmuls: int
+    t_filter: float
+    t_qr: float
+    t_rr: float
+    t_resid: float
+
+
+@dataclass
+class SolveReport:
+    """Solve statistics (core.py:134-165)."""
+
+    n: int = 0
+    nev: int = 0
+    iterations: list = field(default_factory=list)
+    setup_matmuls: int = 0
+    total_matmuls: int = 0
+    upper_bound: float = 0.0
+    est_lam1: float = 0.0
+    est_lam_next: float = 0.0
+    t_lanczos: float = 0.0
+    t_filter: float = 0.0
+    t_qr: float = 0.0
+    t_rr: float = 0.0
+    t_resid: float = 0.0
+    t_total: float = 0.0
+    converged: bool = False
+    # B200 build: filter FLOPs actually executed (8 n^2 m sum filtered_cols)
+    filter_flops: float = 0.0
+
+    @property
+    def outer_iterations(self):
+        return len(self.iterations)
+
+    @property
+    def converged_counts(self):
+        return [it.converged for it in self.iterations]
+
+    @property
+    def filter_tflops(self):
+        return self.filter_flops / self.t_filter / 1e12 if self.t_filter > 0 else 0.0
+
+
+# ----------------------------------------------------------------------
+# helpers
+
+
+def _rng(seed):
+    return seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
+
+
+def _hermitian(H, device=None):
+    """Device-resident Hermitian operator for H (no re-validation for wrappers)."""
+    if isinstance(H, HermitianDenseMatrix):
+        return H
+    if hasattr(H, "entries") and not isinstance(H, (VectorBlock, LowerTriangularFactor)):
+        H = H.entries  # e.g. the reference's own HermitianDenseMatrix
+    a = np.asarray(H, dtype=np.complex128)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ContractViolation(f"expected a square matrix, got shape {a.shape}")
+    # the reference uses a raw ndarray as is (core.py:404 `_asarray`): upload unchanged
+    block = dev.to_device(a, device if device is not None else default_device())
+    return HermitianDenseMatrix.from_device(block, trusted=True)
+
+
+def _host_block(x):
+    if isinstance(x, (VectorBlock, LowerTriangularFactor, HermitianDenseMatrix)):
+        return x.entries
+    if hasattr(x, "entries"):
+        return np.asarray(x.entries, dtype=np.complex128)
+    return np.asarray(x, dtype=np.complex128)
+
+
+def _rand_cols(rng, n, s):
+    return rng.standard_normal((n, s)) + 1j * rng.standard_normal((n, s))
+
+
+# ----------------------------------------------------------------------
+# reduction to standard form (core.py:172-195)
+
+
+def reduce_to_standard(A, L):
+    """H = L^-1 A L^-H, re-symmetrised (core.py:172-188): triangular inverse
+    plus two DMMA GEMMs; the result stays on the device."""
+    lfac = L if isinstance(L, LowerTriangularFactor) else LowerTriangularFactor(L)
+    ab = A.device_block() if isinstance(A, HermitianDenseMatrix) else to_block(_host_block(A))
+    if dev.rows(ab) != lfac.n:
+        raise ContractViolation(f"order mismatch: A is {(dev.rows(ab), dev.cols(ab))}, "
+                                f"L is {(lfac.n, lfac.n)}")
+    return HermitianDenseMatrix(_reduce_block(ab, lfac), rtol=1e-8)
+
+
+def _reduce_block(ab, lfac, linv=None):
+    eng = engine(ab.device)
+    n = dev.rows(ab)
+    if linv is None:
+        linv = dev.empty(n, n, ab.device)
+        eng.trtri_lower(lfac.device_block(ab.device), linv)
+    w = dev.empty(n, n, ab.device)
+    eng.zgemm("N", "N", n, n, n, 1.0, linv, ab, 0.0, w)
+    h = dev.empty(n, n, ab.device)
+    eng.zgemm("N", "C", n, n, n, 1.0, w, linv, 0.0, h)
+    return h
+
+
+def back_transform(Y, L):
+    """C = L^-H Y (core.py:191-195)."""
+    yb = Y.device_block() if isinstance(Y, VectorBlock) else to_block(_host_block(Y))
+    return VectorBlock(solve_triangular_device(L, yb, side="left", adjoint=True))
+
+
+# ----------------------------------------------------------------------
+# building blocks
+
+
+def lanczos_upper_bound(H, k, seed=0):
+    """Upper bound for lambda_max(H) from k Lanczos steps (core.py:202-256).
+    The start vector is drawn from ``seed``'s Generator exactly like the
+    reference; the k GEMVs, dots and reorthogonalisation run on the GPU."""
+    k = int(k)
+    if k < 2:
+        raise ContractViolation(f"lanczos steps must be >= 2, got {k}")
+    hm = _hermitian(H)
+    rng = _rng(seed)
+    return _lanczos(hm, k, rng)
+
+
+def _lanczos(hm, k, rng):
+    n = hm.n
+    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    hb = hm.device_block()
+    vb = dev.to_device(v, hb.device)
+    bound, _, _ = engine(hb.device).lanczos_bound(hb, vb, min(k, n))
+    _count_products(min(k, n))
+    return bound
+
+
+def chebyshev_filter(H, Y, spec):
+    """p_m(H) Y with the scaled Chebyshev recurrence (core.py:287-311)."""
+    if not isinstance(spec, FilterSpec):
+        if all(hasattr(spec, f) for f in ("degree", "a", "b", "lam_ref")):
+            spec = FilterSpec(spec.degree, spec.a, spec.b, spec.lam_ref)
+        else:
+            raise ContractViolation("spec must be a FilterSpec")
+    if spec.lam_ref >= spec.a:
+        raise FilterDegenerate(
+            f"lam_ref = {spec.lam_ref} lies inside the unwanted interval [{spec.a}, {spec.b}]; "
+            f"wanted and unwanted intervals overlap (a larger buffer improves the "
+            f"lambda_nev+1 estimate)")
+    hm = _hermitian(H)
+    if isinstance(Y, VectorBlock):
+        yb = Y.device_block(hm.device_block().device).clone()
+    else:
+        y = _host_block(Y)
+        y2d = y if y.ndim == 2 else y.reshape(-1, 1)
+        if y2d.shape[0] != hm.n:
+            raise ContractViolation(
+                f"filter operand mismatch: H is {(hm.n, hm.n)}, Y has {y2d.shape[0]} rows")
+        yb = dev.to_device(y2d, hm.device_block().device)
+    if dev.rows(yb) != hm.n:
+        raise ContractViolation(f"filter operand mismatch: H is {(hm.n, hm.n)}, Y has {dev.rows(yb)} rows")
+    w = torch.empty_like(yb)
+    out = engine(yb.device).filter(hm.device_block(), yb, w, spec.degree, spec.a, spec.b,
+                                   spec.lam_ref)
+    _count_products(spec.degree * dev.cols(yb))
+    return VectorBlock(out)
+
+
+def rayleigh_ritz(H, Q):
+    """Ritz values (ascending) and rotated block Q W (core.py:333-344)."""
+    hm = _hermitian(H)
+    if isinstance(Q, VectorBlock):
+        qb = Q.device_block(hm.device_block().device)
+        if not Q.orthonormal:
+            from .linalg import _orth_deviation
+            devn = _orth_deviation(qb)
+            if devn > 1e-10 * np.sqrt(Q.s):
+                raise ContractViolation(f"rayleigh_ritz requires orthonormal columns, deviation {devn:.3e}")
+    else:
+        qb = dev.to_device(_host_block(Q), hm.device_block().device)
+    n, k = dev.rows(qb), dev.cols(qb)
+    hq, z, hz = (dev.empty(n, k, qb.device) for _ in range(3))
+    w = engine(qb.device).rayleigh_ritz(hm.device_block(), qb, hq, z, hz)
+    _count_products(k)
+    return w, VectorBlock(z, orthonormal=True)
+
+
+def residuals(H, Y, lambdas):
+    """||H y_i - lambda_i y_i||_2 per column (core.py:347-358)."""
+    hm = _hermitian(H)
+    if isinstance(Y, VectorBlock):
+        yb = Y.device_block(hm.device_block().device)
+    else:
+        y = _host_block(Y)
+        y2d = y if y.ndim == 2 else y.reshape(-1, 1)
+        yb = dev.to_device(y2d, hm.device_block().device)
+    lam = np.asarray(lambdas, dtype=np.float64).ravel()
+    if lam.shape[0] != dev.cols(yb):
+        raise ContractViolation(f"{lam.shape[0]} eigenvalues for {dev.cols(yb)} columns")
+    n, k = dev.rows(yb), dev.cols(yb)
+    eng = engine(yb.device)
+    hy = dev.empty(n, k, yb.device)
+    eng.zgemm("N", "N", n, k, n, 1.0, hm.device_block(), yb, 0.0, hy)
+    _count_products(k)
+    return eng.residual_norms(hy, yb, lam)
+
+
+# ----------------------------------------------------------------------
+# the solver
+
+
+class _Workspace:
+    """Device buffers of one solve, reused across outer iterations."""
+
+    def __init__(self, n, s_tot, nev, device):
+        self.n, self.s, self.nev = n, s_tot, nev
+        self.fa = dev.empty(n, s_tot, device)
+        self.fb = dev.empty(n, s_tot, device)
+        self.hq = dev.empty(n, s_tot, device)
+        self.z = dev.empty(n, s_tot, device)
+        self.hz = dev.empty(n, s_tot, device)
+        self.locked = dev.empty(n, nev, device)
+
+
+class DeviceSolver:
+    """One ChFSI solve on a device-resident H (core.py:385-546)."""
+
+    def __init__(self, hm, config, device=None):
+        self.hm = hm
+        self.cfg = config
+        self.hb = hm.device_block(device)
+        self.device = self.hb.device
+        self.eng = engine(self.device)
+        self.n = hm.n
+
+    # -- phases -------------------------------------------------------
+    def _filter(self, active, out_other, a_edge, b_up, lam_ref):
+        """Filter the active block in place (active is clobbered); returns the
+        tensor with p_m(H) active: either ``active`` or ``out_other``."""
+        return self.eng.filter(self.hb, active, out_other, self.cfg.degree, a_edge, b_up, lam_ref)
+
+    def _orthonormalize(self, f, locked, t, q, rng):
+        """core.py:365-382 with rank-collapse replacement from the host RNG."""
+        n = self.n
+        for _ in range(dev.cols(f) + 2):
+            try:
+                self.eng.orthonormalize(f, locked, t, q, rank_tol=1e-14)
+                return q
+            except RankDeficient as exc:
+                col = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+                f[exc.column].copy_(torch.from_numpy(col).to(self.device))
+        raise RankDeficient(0)
+
+    def _sync(self):
+        self.eng.synchronize()
+
+    # -- driver -------------------------------------------------------
+    def run(self, Y0, prior, rng):
+        cfg = self.cfg
+        n, nev = self.n, cfg.nev
+        s_tot = nev + cfg.buffer_cols
+        ws = _Workspace(n, s_tot, nev, self.device)
+        report = SolveReport(n=n, nev=nev)
+        t_start = time.perf_counter()
+
+        if Y0 is None or (isinstance(Y0, str) and Y0 == "random"):
+            ws.z.copy_(dev.to_device(_rand_cols(rng, n, s_tot), self.device))
+        elif isinstance(Y0, torch.Tensor):
+            ws.z.copy_(Y0)
+        else:
+            ws.z.copy_(dev.to_device(Y0, self.device))
+
+        t0 = time.perf_counter()
+        b_up = _lanczos(self.hm, cfg.lanczos_steps, rng)
+        report.t_lanczos = time.perf_counter() - t0
+        report.setup_matmuls += min(cfg.lanczos_steps, n)
+        report.upper_bound = b_up
+
+        if prior is not None:
+            lam_ref, a_edge = float(prior[0]), float(prior[1])
+        else:
+            # bootstrap: one unfiltered Rayleigh-Ritz pass on the start block
+            t0 = time.perf_counter()
+            q = self._orthonormalize(ws.z, None, ws.hq, ws.fa, rng)
+            w = self.eng.rayleigh_ritz(self.hb, q, ws.hq, ws.z, ws.hz)
+            _count_products(s_tot)
+            report.t_rr += time.perf_counter() - t0
+            report.setup_matmuls += s_tot
+            lam_ref, a_edge = float(w[0]), float(w[nev])
+            if cfg.interval == "block_top":
+                a_edge = float(w[-1])
+
+        locked_vals = []
+        nl = 0
+        act = ws.z[:s_tot]  # the unconverged block, a contiguous column range of Z
+        for it in range(1, cfg.max_outer_iters + 1):
+            if not lam_ref < a_edge:
+                raise FilterDegenerate(
+                    f"lambda_1 estimate {lam_ref} >= lambda_nev+1 estimate {a_edge}; "
+                    f"interval placement ill-posed (increase buffer)")
+            if not a_edge < b_up:
+                b_up = a_edge + max(1.0, abs(a_edge)) * 1e-8
+            ncols = dev.cols(act)
+
+            t0 = time.perf_counter()
+            f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref)
+            self._sync()
+            tf = time.perf_counter() - t0
+            _count_products(cfg.degree * ncols)
+            report.filter_flops += 8.0 * n * n * cfg.degree * ncols
+
+            t0 = time.perf_counter()
+            q = self._orthonormalize(f, ws.locked[:nl] if nl else None, ws.hq[:ncols],
+                                     ws.fa[:ncols], rng)
+            self._sync()
+            tq = time.perf_counter() - t0
+
+            t0 = time.perf_counter()
+            w = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols], ws.hz[:ncols])
+            _count_products(ncols)
+            trr = time.perf_counter() - t0
+
+            t0 = time.perf_counter()
+            res = self.eng.residual_norms(ws.hz[:ncols], ws.z[:ncols], w)
+            tres = time.perf_counter() - t0
+
+            kk = 0
+            while kk < len(w) and res[kk] < cfg.tol and len(locked_vals) < nev:
+                locked_vals.append(float(w[kk]))
+                kk += 1
+            if kk:
+                ws.locked[nl:nl + kk].copy_(ws.z[:kk])
+                nl += kk
+            act = ws.z[kk:ncols]
+
+            unconv = res[kk:]
+            report.iterations.append(IterationStat(
+                iteration=it, filtered_cols=ncols, converged=len(locked_vals),
+                max_resid=float(unconv.max()) if unconv.size else 0.0,
+                min_resid=float(unconv.min()) if unconv.size else 0.0,
+                matmuls=(cfg.degree + 1) * ncols,
+                t_filter=tf, t_qr=tq, t_rr=trr, t_resid=tres))
+            report.t_filter += tf
+            report.t_qr += tq
+            report.t_rr += trr
+            report.t_resid += tres
+
+            comb = np.sort(np.concatenate([locked_vals, w[kk:]]))
+            lam_ref = float(comb[0])
+            a_edge = float(comb[nev])
+            if cfg.interval == "block_top":
+                a_edge = float(comb[-1])
+            report.est_lam1 = lam_ref
+            report.est_lam_next = float(comb[nev])
+            if len(locked_vals) >= nev:
+                break
+
+        report.total_matmuls = report.setup_matmuls + sum(i.matmuls for i in report.iterations)
+        vecs = ws.locked[:nl]
+        if len(locked_vals) < nev:
+            report.t_total = time.perf_counter() - t_start
+            raise NotConverged(
+                f"{len(locked_vals)}/{nev} pairs converged after {cfg.max_outer_iters} outer "
+                f"iterations", np.asarray(locked_vals),
+                VectorBlock(vecs.clone()) if nl else dev.to_host(vecs), report)
+
+        vals = np.asarray(locked_vals)
+        t0 = time.perf_counter()
+        self.eng.zgemm("N", "N", n, nev, n, 1.0, self.hb, vecs, 0.0, ws.hq[:nev])
+        _count_products(nev)
+        final_res = self.eng.residual_norms(ws.hq[:nev], vecs, vals)
+        report.t_resid += time.perf_counter() - t0
+        report.total_matmuls += nev
+        report.t_total = time.perf_counter() - t_start
+        out = vecs.clone()
+        del ws
+        if np.any(final_res >= cfg.tol):
+            raise NotConverged(f"final residual re-check failed: max {final_res.max():.3e}",
+                               vals, VectorBlock(out), report)
+        report.converged = True
+        return vals, VectorBlock(out, orthonormal=True), report
+
+
+def chfsi_solve(H, Y0, config, prior=None, seed=0):
+    """Run ChFSI on a standard Hermitian problem (core.py:385-546).
+
+    Same signature, return types, report fields, RNG order and exceptions
+    as the reference; arithmetic on the GPU.
+    """
+    config = _as_config(config)
+    if isinstance(H, HermitianDenseMatrix):
+        n = H.n
+    else:
+        hh = H.entries if hasattr(H, "entries") else np.asarray(H)
+        if hh.ndim != 2 or hh.shape[0] != hh.shape[1]:
+            raise ContractViolation(f"expected a square matrix, got shape {hh.shape}")
+        n = hh.shape[0]
+    nev = config.nev
+    s_tot = nev + config.buffer_cols
+    if s_tot > n:
+        raise ContractViolation(f"nev + buffer = {s_tot} exceeds the matrix order {n}")
+    rng = _rng(seed)
+    y0 = None
+    if Y0 is None or (isinstance(Y0, str) and Y0 == "random"):
+        y0 = None
+    elif isinstance(Y0, VectorBlock) and Y0._dev is not None:
+        if (Y0.n, Y0.s) != (n, s_tot):
+            raise ContractViolation(f"start block must be {n} x {s_tot}, got {(Y0.n, Y0.s)}")
+        y0 = Y0._dev
+    else:
+        y = _host_block(Y0)
+        if y.ndim != 2 or y.shape != (n, s_tot):
+            raise ContractViolation(f"start block must be {n} x {s_tot}, got {y.shape}")
+        y0 = y
+    hm = _hermitian(H)
+    return DeviceSolver(hm, config).run(y0, prior, rng)
+
+
+def solve_generalized(A, B, Y0, config, prior=None, seed=0):
+    """A c = lambda B c for the nev lowest pairs (core.py:549-569):
+    B = L L^H (cuSOLVER zpotrf), H = L^-1 A L^-H (triangular inverse + DMMA
+    GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors."""
+    config = _as_config(config)
+    ab = A.device_block() if isinstance(A, HermitianDenseMatrix) else None
+    bb = B.device_block() if isinstance(B, HermitianDenseMatrix) else None
+    ah = None if ab is not None else _host_block(A)
+    bh = None if bb is not None else _host_block(B)
+    ashape = (A.n, A.n) if ab is not None else ah.shape
+    bshape = (B.n, B.n) if bb is not None else bh.shape
+    if tuple(ashape) != tuple(bshape):
+        raise ContractViolation(f"A and B orders differ: {tuple(ashape)} vs {tuple(bshape)}")
+    lfac = cholesky_factor(B if bb is not None else bh)
+    d = lfac.device_block().device
+    if ab is None:
+        ab = dev.to_device(ah, d)
+    n = dev.rows(ab)
+    eng = engine(d)
+    linv = dev.empty(n, n, d)
+    eng.trtri_lower(lfac.device_block(), linv)
+    hm = HermitianDenseMatrix(_reduce_block(ab, lfac, linv), rtol=1e-8)
+    y0 = Y0
+    if Y0 is not None and not (isinstance(Y0, str) and Y0 == "random"):
+        yb = Y0.device_block(d) if isinstance(Y0, VectorBlock) else to_block(_host_block(Y0), d)
+        fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
+        eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd)
+        y0 = VectorBlock(fwd)
+    lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed)
+    c = dev.empty(n, yv.s, d)
+    eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c)
+    return lam, VectorBlock(c), report

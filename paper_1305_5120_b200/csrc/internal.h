@@ -1,0 +1,106 @@
+// Internal (C++) interface shared by the translation units of libchfsi_b200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+namespace chfsi {
+
+// Status codes returned through the C ABI (include/chfsi_b200.h).
+enum Status : int {
+  OK = 0,
+  ERR_ARG = -1,        // contract violation on arguments
+  ERR_CUDA = -2,       // CUDA runtime failure
+  ERR_CUSOLVER = -3,   // cuSOLVER failure
+  ERR_NOT_PD = -4,     // Cholesky pivot failure (detail = 1-based pivot)
+  ERR_RANK = -5,       // rank collapse (detail = 0-based column)
+  ERR_NOMEM = -6,
+};
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  // grow-only scratch arenas (stream-ordered reuse is safe: one stream)
+  void* scratch[8] = {nullptr};
+  size_t scratch_bytes[8] = {0};
+  int* d_info = nullptr;
+  double* h_pinned = nullptr;   // small pinned host staging
+  size_t h_pinned_bytes = 0;
+  int sm_count = 148;
+  // launch counter: kernels this library launched since the last reset
+  long long launches = 0;
+};
+
+// scratch slots
+enum Slot : int {
+  SLOT_SPLITK = 0,  // split-K partials
+  SLOT_SMALL = 1,   // k x k Gram / eigvecs
+  SLOT_SMALL2 = 2,  // k x k inverse factors
+  SLOT_PROJ = 3,    // locked-projection coefficients nl x k
+  SLOT_SOLVER = 4,  // cuSOLVER workspace
+  SLOT_VEC = 5,     // small vectors (eigvalues, diagonals, norms)
+  SLOT_TRI = 6,     // triangular-inverse temporaries
+  SLOT_LANCZOS = 7, // Lanczos basis
+};
+
+void set_error(const std::string& msg);
+void* scratch(Handle* h, int slot, size_t bytes);  // nullptr on failure (error set)
+double* pinned(Handle* h, size_t bytes);
+
+#define CHFSI_CUDA(call)                                                            \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      ::chfsi::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));      \
+      return ::chfsi::ERR_CUDA;                                                     \
+    }                                                                               \
+  } while (0)
+
+#define CHFSI_CHECK_LAUNCH()                                                        \
+  do {                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                            \
+    if (e_ != cudaSuccess) {                                                        \
+      ::chfsi::set_error(std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+      return ::chfsi::ERR_CUDA;                                                     \
+    }                                                                               \
+  } while (0)
+
+#define CHFSI_TRY(expr)            \
+  do {                             \
+    int s_ = (expr);               \
+    if (s_ != ::chfsi::OK) return s_; \
+  } while (0)
+
+// ---- GEMM (zgemm.cu) ----
+// C = alpha op(A) op(B) + beta C, complex128 column-major.
+int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, double2 alpha,
+          const double2* A, long long lda, const double2* B, long long ldb, double2 beta,
+          double2* C, long long ldc);
+// One fused Chebyshev degree step: C = alpha*A*Y1 + beta*Y1 + gamma*Y0 (Y0 may be null,
+// C may alias Y0). A is M x M, Y1/Y0/C are M x N.
+int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
+                      const double2* Y1, long long ld1, double alpha, double beta,
+                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc);
+
+// ---- misc kernels (kernels.cu) ----
+int residual_norms(Handle* h, long long n, long long k, const double2* HY, long long ldhy,
+                   const double2* Y, long long ldy, const double* lam_dev, double* res_dev);
+int zdotc_cols(Handle* h, long long n, long long k, const double2* X, long long ldx,
+               const double2* Y, long long ldy, double2* out_dev);
+int hermitian_norms(Handle* h, long long n, const double2* A, long long lda, double* out2_dev);
+int hermitize(Handle* h, long long n, double2* A, long long lda);
+int clean_lower_factor(Handle* h, long long n, double2* L, long long ldl);
+int trtri_lower(Handle* h, long long n, const double2* L, long long ldl, double2* X, long long ldx);
+int zaxpby_cols(Handle* h, long long n, long long k, double2 alpha, const double2* X,
+                long long ldx, double2 beta, double2* Y, long long ldy);
+int get_real_diag(Handle* h, long long n, const double2* A, long long lda, double* out_dev);
+int zcopy2d(Handle* h, long long rows, long long cols, const double2* src, long long lds,
+            double2* dst, long long ldd);
+int shift_diag(Handle* h, long long n, double2* A, long long lda, double shift);
+
+}  // namespace chfsi

@@ -1,0 +1,304 @@
+// Composite ChFSI phases built on the DMMA GEMM and helper kernels.
+//
+//   filter          core.py:263-284 (_filter_raw)
+//   lanczos_bound   core.py:202-256 (lanczos_upper_bound)
+//   orthonormalize  core.py:365-382 (_qr_against_locked): CGS2 against the
+//                   locked block, then CholQR2 (shifted CholQR3 when the first
+//                   Cholesky breaks down); rank test on |prod diag R| like
+//                   linalg.py:284-288 / core.py:374-377.
+//   rayleigh_ritz   core.py:318-330 (_rr_raw); cuSOLVER zheevd for the k x k
+//                   eigenproblem (replaces the numba Jacobi _jacobi.py:14-80).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace chfsi {
+
+namespace {
+const double2 ONE = {1.0, 0.0};
+const double2 ZERO = {0.0, 0.0};
+const double2 MONE = {-1.0, 0.0};
+
+#define CHFSI_SOLVER(call)                                                          \
+  do {                                                                              \
+    cusolverStatus_t s_ = (call);                                                   \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                            \
+      ::chfsi::set_error(std::string(#call) + ": cusolver status " + std::to_string((int)s_)); \
+      return ::chfsi::ERR_CUSOLVER;                                                 \
+    }                                                                               \
+  } while (0)
+
+}  // namespace
+
+int potrf_lower(Handle* h, long long n, double2* A, long long lda, int* info_host) {
+  int lwork = 0;
+  CHFSI_SOLVER(cusolverDnZpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, (int)n,
+                                           (cuDoubleComplex*)A, (int)lda, &lwork));
+  void* work = scratch(h, SLOT_SOLVER, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+  if (!work) return ERR_NOMEM;
+  CHFSI_SOLVER(cusolverDnZpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, (int)n, (cuDoubleComplex*)A,
+                                (int)lda, (cuDoubleComplex*)work, lwork, h->d_info));
+  h->launches++;
+  CHFSI_CUDA(cudaMemcpyAsync(info_host, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  return OK;
+}
+
+int heevd(Handle* h, long long n, double2* A, long long lda, double* w_dev) {
+  int lwork = 0;
+  CHFSI_SOLVER(cusolverDnZheevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                           CUBLAS_FILL_MODE_LOWER, (int)n, (cuDoubleComplex*)A,
+                                           (int)lda, w_dev, &lwork));
+  void* work = scratch(h, SLOT_SOLVER, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+  if (!work) return ERR_NOMEM;
+  CHFSI_SOLVER(cusolverDnZheevd(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                (int)n, (cuDoubleComplex*)A, (int)lda, w_dev,
+                                (cuDoubleComplex*)work, lwork, h->d_info));
+  h->launches++;
+  int info = 0;
+  CHFSI_CUDA(cudaMemcpyAsync(&info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  if (info != 0) {
+    set_error("zheevd failed to converge, info=" + std::to_string(info));
+    return ERR_CUSOLVER;
+  }
+  return OK;
+}
+
+int filter(Handle* h, long long n, long long k, int degree, double a, double b, double lam_ref,
+           const double2* H, long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
+           int* result_in_w) {
+  if (degree < 1) {
+    set_error("filter degree must be >= 1");
+    return ERR_ARG;
+  }
+  const double c = (a + b) / 2.0;
+  const double e = (b - a) / 2.0;
+  const double sigma1 = e / (lam_ref - c);
+  double sigma = sigma1;
+  // y1 = sigma1/e * H y - c*sigma1/e * y
+  CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, Y, ldy, sigma1 / e, -c * sigma1 / e, nullptr, 0,
+                              0.0, W, ldw));
+  double2* prev = Y;
+  long long ldp = ldy;
+  double2* cur = W;
+  long long ldc = ldw;
+  for (int j = 1; j < degree; ++j) {
+    const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+    const double scale = 2.0 * sigma_new / e;
+    // y2 = scale*(H y1) - c*scale*y1 - sigma*sigma_new*y0, written over y0
+    CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, scale, -c * scale, prev, ldp,
+                                -(sigma * sigma_new), prev, ldp));
+    std::swap(prev, cur);
+    std::swap(ldp, ldc);
+    sigma = sigma_new;
+  }
+  *result_in_w = (cur == W) ? 1 : 0;
+  return OK;
+}
+
+// eigenvalues of a real symmetric tridiagonal (diag d, offdiag e) by cyclic Jacobi
+static void sym_eig_small(int m, const double* d, const double* e, double* lam) {
+  std::vector<double> A((size_t)m * m, 0.0);
+  for (int i = 0; i < m; ++i) {
+    A[i * m + i] = d[i];
+    if (i + 1 < m) A[i * m + i + 1] = A[(i + 1) * m + i] = e[i];
+  }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, fro = 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        fro += A[i * m + j] * A[i * m + j];
+        if (i != j) off += A[i * m + j] * A[i * m + j];
+      }
+    if (off <= 1e-32 * fro || off == 0.0) break;
+    for (int p = 0; p < m - 1; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = A[p * m + q];
+        if (apq == 0.0) continue;
+        const double tau = (A[q * m + q] - A[p * m + p]) / (2.0 * apq);
+        const double t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
+        const double cs = 1.0 / std::sqrt(1.0 + t * t), sn = t * cs;
+        for (int r = 0; r < m; ++r) {
+          const double arp = A[r * m + p], arq = A[r * m + q];
+          A[r * m + p] = cs * arp - sn * arq;
+          A[r * m + q] = sn * arp + cs * arq;
+        }
+        for (int r = 0; r < m; ++r) {
+          const double apr = A[p * m + r], aqr = A[q * m + r];
+          A[p * m + r] = cs * apr - sn * aqr;
+          A[q * m + r] = sn * apr + cs * aqr;
+        }
+      }
+  }
+  for (int i = 0; i < m; ++i) lam[i] = A[i * m + i];
+  std::sort(lam, lam + m);
+}
+
+int lanczos_bound(Handle* h, long long n, int k, const double2* H, long long ldh,
+                  const double2* v0, double* alphas, double* betas, int* steps, double* bound) {
+  if (k < 2) {
+    set_error("lanczos steps must be >= 2");
+    return ERR_ARG;
+  }
+  if (k > n) k = (int)n;
+  double2* basis = (double2*)scratch(h, SLOT_LANCZOS, (size_t)n * (k + 1) * sizeof(double2));
+  double2* vec = (double2*)scratch(h, SLOT_VEC, (size_t)(2 * k + 8) * sizeof(double2));
+  if (!basis || !vec) return ERR_NOMEM;
+  double2* w = basis + (long long)n * k;
+  double2* coeff = vec + 2;
+  double* hst = pinned(h, 4 * sizeof(double));
+  if (!hst) return ERR_NOMEM;
+  CHFSI_TRY(zcopy2d(h, n, 1, v0, n, basis, n));
+  int j = 0;
+  for (; j < k; ++j) {
+    double2* bj = basis + (long long)j * n;
+    CHFSI_TRY(zgemm(h, OP_N, OP_N, n, 1, n, ONE, H, ldh, bj, n, ZERO, w, n));
+    CHFSI_TRY(zdotc_cols(h, n, 1, bj, n, w, n, vec));
+    CHFSI_CUDA(cudaMemcpyAsync(hst, vec, sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+    const double aj = hst[0];
+    alphas[j] = aj;
+    CHFSI_TRY(zaxpby_cols(h, n, 1, make_double2(-aj, 0.0), bj, n, ONE, w, n));
+    if (j > 0)
+      CHFSI_TRY(zaxpby_cols(h, n, 1, make_double2(-betas[j - 1], 0.0), bj - n, n, ONE, w, n));
+    // full reorthogonalisation: w -= B (B^H w)
+    CHFSI_TRY(zgemm(h, OP_C, OP_N, j + 1, 1, n, ONE, basis, n, w, n, ZERO, coeff, j + 1));
+    CHFSI_TRY(zgemm(h, OP_N, OP_N, n, 1, j + 1, MONE, basis, n, coeff, j + 1, ONE, w, n));
+    CHFSI_TRY(zdotc_cols(h, n, 1, w, n, w, n, vec));
+    CHFSI_CUDA(cudaMemcpyAsync(hst, vec, sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+    const double bj_norm = std::sqrt(hst[0]);
+    betas[j] = bj_norm;
+    if (bj_norm < 1e-14 || j == k - 1) {
+      ++j;
+      break;
+    }
+    CHFSI_TRY(zaxpby_cols(h, n, 1, make_double2(1.0 / bj_norm, 0.0), w, n, ZERO, bj + n, n));
+  }
+  *steps = j;
+  std::vector<double> lam(j);
+  sym_eig_small(j, alphas, betas, lam.data());
+  const double guard = 4.0 * j * 2.220446049250313e-16 * std::max(std::fabs(lam[0]), std::fabs(lam[j - 1]));
+  *bound = lam[j - 1] + betas[j - 1] + guard;
+  return OK;
+}
+
+// One Cholesky-QR pass: out = X R^-1 where X^H X = R^H R (+ shift I).
+// diag_host receives the real diagonal of R. Returns ERR_NOT_PD (detail=pivot) on failure.
+static int cholqr_pass(Handle* h, long long n, long long k, const double2* X, long long ldx,
+                       double2* out, long long ldo, double shift, double* diag_host,
+                       int* pivot) {
+  double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
+  double2* Li = (double2*)scratch(h, SLOT_SMALL2, (size_t)k * k * sizeof(double2));
+  double* dv = (double*)scratch(h, SLOT_VEC, (size_t)(k + 8) * sizeof(double));
+  if (!G || !Li || !dv) return ERR_NOMEM;
+  CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, X, ldx, X, ldx, ZERO, G, k));
+  CHFSI_TRY(hermitize(h, k, G, k));
+  if (shift != 0.0) CHFSI_TRY(shift_diag(h, k, G, k, shift));
+  int info = 0;
+  CHFSI_TRY(potrf_lower(h, k, G, k, &info));
+  if (info != 0) {
+    *pivot = info;
+    return ERR_NOT_PD;
+  }
+  CHFSI_TRY(get_real_diag(h, k, G, k, dv));
+  CHFSI_CUDA(cudaMemcpyAsync(diag_host, dv, k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_TRY(trtri_lower(h, k, G, k, Li, k));
+  // R^-1 = (L^H)^-1 = (L^-1)^H
+  CHFSI_TRY(zgemm(h, OP_N, OP_C, n, k, k, ONE, X, ldx, Li, k, ZERO, out, ldo));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  return OK;
+}
+
+int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ldf,
+                   const double2* Lk, long long ldl, long long nl, double2* T, long long ldt,
+                   double2* Q, long long ldq, double rank_rel_tol, long long* bad_col,
+                   double* fro_out) {
+  *bad_col = -1;
+  if (k <= 0) return OK;
+  if (nl > 0) {
+    double2* P = (double2*)scratch(h, SLOT_PROJ, (size_t)nl * k * sizeof(double2));
+    if (!P) return ERR_NOMEM;
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2
+      CHFSI_TRY(zgemm(h, OP_C, OP_N, nl, k, n, ONE, Lk, ldl, F, ldf, ZERO, P, nl));
+      CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, nl, MONE, Lk, ldl, P, nl, ONE, F, ldf));
+    }
+  }
+  std::vector<double> d1(k), d2(k), d3(k);
+  // ||W||_F via column dots (deterministic), summed on the host in fixed order
+  {
+    double2* dots = (double2*)scratch(h, SLOT_SMALL2, (size_t)k * sizeof(double2));
+    if (!dots) return ERR_NOMEM;
+    CHFSI_TRY(zdotc_cols(h, n, k, F, ldf, F, ldf, dots));
+    std::vector<double2> hd(k);
+    CHFSI_CUDA(cudaMemcpyAsync(hd.data(), dots, k * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+    double s = 0.0;
+    for (long long j = 0; j < k; ++j) s += hd[j].x;
+    *fro_out = std::sqrt(s);
+  }
+  const double fro = *fro_out;
+  int pivot = 0;
+  int st = cholqr_pass(h, n, k, F, ldf, T, ldt, 0.0, d1.data(), &pivot);
+  bool shifted = false;
+  if (st == ERR_NOT_PD) {
+    // shifted CholQR (Fukaya et al.): s = 11 (n k + k (k+1)) u ||F||^2
+    const double u = 1.1102230246251565e-16;
+    const double s = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro * fro;
+    st = cholqr_pass(h, n, k, F, ldf, T, ldt, s, d1.data(), &pivot);
+    shifted = true;
+  }
+  if (st == ERR_NOT_PD) {
+    *bad_col = pivot - 1;
+    set_error("rank collapse in column " + std::to_string(pivot - 1));
+    return ERR_RANK;
+  }
+  CHFSI_TRY(st);
+  st = cholqr_pass(h, n, k, T, ldt, Q, ldq, 0.0, d2.data(), &pivot);
+  if (st == ERR_NOT_PD) {
+    *bad_col = pivot - 1;
+    set_error("rank collapse in column " + std::to_string(pivot - 1));
+    return ERR_RANK;
+  }
+  CHFSI_TRY(st);
+  if (shifted) {
+    st = cholqr_pass(h, n, k, Q, ldq, T, ldt, 0.0, d3.data(), &pivot);
+    if (st == ERR_NOT_PD) {
+      *bad_col = pivot - 1;
+      set_error("rank collapse in column " + std::to_string(pivot - 1));
+      return ERR_RANK;
+    }
+    CHFSI_TRY(st);
+    CHFSI_TRY(zcopy2d(h, n, k, T, ldt, Q, ldq));
+  }
+  for (long long j = 0; j < k; ++j) {
+    double r = std::fabs(d1[j] * d2[j]);
+    if (shifted) r *= std::fabs(d3[j]);
+    if (r < rank_rel_tol * fro) {
+      *bad_col = j;
+      set_error("rank collapse in column " + std::to_string(j));
+      return ERR_RANK;
+    }
+  }
+  return OK;
+}
+
+int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long long ldh,
+                  const double2* Q, long long ldq, double2* HQ, long long ldhq, double2* Z,
+                  long long ldz, double2* HZ, long long ldhz, double* w_dev) {
+  double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
+  if (!G) return ERR_NOMEM;
+  CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, Q, ldq, ZERO, HQ, ldhq));
+  CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, Q, ldq, HQ, ldhq, ZERO, G, k));
+  CHFSI_TRY(hermitize(h, k, G, k));
+  CHFSI_TRY(heevd(h, k, G, k, w_dev));
+  CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, k, ONE, Q, ldq, G, k, ZERO, Z, ldz));
+  CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, k, ONE, HQ, ldhq, G, k, ZERO, HZ, ldhz));
+  return OK;
+}
+
+}  // namespace chfsi

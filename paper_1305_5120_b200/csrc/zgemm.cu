@@ -1,0 +1,252 @@
+// Tile-configuration dispatch for the DMMA complex GEMM (zgemm.cuh).
+//
+// A small cost model picks, per call, the CTA tile (64x64, 64x32, 64x16 or
+// 32x16) and a deterministic split-K factor so that the grid fills the 148
+// SMs in whole waves: the filter's tail blocks are only nex+few columns wide
+// (SURVEY.md section 0.5), where a single 64-row tile column would leave
+// most SMs idle. Split-K partials are reduced in fixed z order, so results
+// are bit-identical run to run (reference criterion 7, test_acceptance.py:199).
+#include <algorithm>
+#include <cmath>
+
+#include "internal.h"
+#include "zgemm.cuh"
+
+namespace chfsi {
+
+__global__ void zgemm_splitk_reduce_kernel(int M, int N, int S, const double2* __restrict__ ws,
+                                           int epi, double2 alpha, double2 beta, double2* C,
+                                           long long ldc, const double2* Y1, long long ld1,
+                                           const double2* Y0, long long ld0, double gamma) {
+  const long long total = (long long)M * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(idx % M);
+    const long long n = idx / M;
+    double xr = 0.0, xi = 0.0;
+    for (int z = 0; z < S; ++z) {
+      const double2 v = ws[(long long)z * total + idx];
+      xr += v.x;
+      xi += v.y;
+    }
+    if (epi == EPI_FILTER) {
+      const double2 y1 = Y1[m + n * ld1];
+      double orr = alpha.x * xr + beta.x * y1.x;
+      double oi = alpha.x * xi + beta.x * y1.y;
+      if (Y0 != nullptr) {
+        const double2 y0 = Y0[m + n * ld0];
+        orr += gamma * y0.x;
+        oi += gamma * y0.y;
+      }
+      C[m + n * ldc] = make_double2(orr, oi);
+    } else {
+      double2 o = make_double2(alpha.x * xr - alpha.y * xi, alpha.x * xi + alpha.y * xr);
+      if (beta.x != 0.0 || beta.y != 0.0) {
+        const double2 c = C[m + n * ldc];
+        o.x += beta.x * c.x - beta.y * c.y;
+        o.y += beta.x * c.y + beta.y * c.x;
+      }
+      C[m + n * ldc] = o;
+    }
+  }
+}
+
+namespace {
+
+struct Cfg {
+  int bm, bn, bk;
+  int threads;
+  int smem;
+  int occ[3];  // per EPI, filled lazily; index by epi
+};
+
+// Kernel pointer table: [cfg][opa][opb][epi]
+using KFn = void (*)(const GemmParams);
+
+template <int BM, int BN, int BK, int WM, int WN, int ST>
+struct CfgT {
+  static constexpr int threads = (BM / WM) * (BN / WN) * 32;
+  template <int OPA, int OPB>
+  static constexpr int smem() { return zgemm_smem_bytes<BM, BN, BK, WM, WN, ST, OPA, OPB>(); }
+  template <int OPA, int OPB, int EPI>
+  static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
+};
+
+constexpr int NCFG = 4;
+// cfg 0: 64x64 (warp 32x32); cfg 1: 64x32 (32x16); cfg 2: 64x16 (16x16); cfg 3: 32x16 (16x8)
+using C0 = CfgT<64, 64, 8, 32, 32, 4>;
+using C1 = CfgT<64, 32, 8, 32, 16, 4>;
+using C2 = CfgT<64, 16, 8, 16, 16, 4>;
+using C3 = CfgT<32, 16, 8, 16, 8, 4>;
+const int kBM[NCFG] = {64, 64, 64, 32};
+const int kBN[NCFG] = {64, 32, 16, 16};
+const int kBK = 8;
+
+struct Entry {
+  KFn fn = nullptr;
+  int threads = 0, smem = 0, occ = 0;
+  bool ready = false;
+};
+Entry g_table[NCFG][2][2][3];
+bool g_table_init = false;
+
+template <class C, int OPA, int OPB, int EPI>
+void put(int ci) {
+  Entry& e = g_table[ci][OPA][OPB][EPI];
+  e.fn = C::template fn<OPA, OPB, EPI>();
+  e.threads = C::threads;
+  e.smem = C::template smem<OPA, OPB>();
+}
+
+template <class C>
+void put_all(int ci) {
+  put<C, 0, 0, 0>(ci); put<C, 0, 0, 1>(ci); put<C, 0, 0, 2>(ci);
+  put<C, 1, 0, 0>(ci); put<C, 1, 0, 2>(ci);
+  put<C, 0, 1, 0>(ci); put<C, 0, 1, 2>(ci);
+  put<C, 1, 1, 0>(ci); put<C, 1, 1, 2>(ci);
+}
+
+int ensure_table() {
+  if (g_table_init) return OK;
+  put_all<C0>(0);
+  put_all<C1>(1);
+  put_all<C2>(2);
+  put_all<C3>(3);
+  for (int c = 0; c < NCFG; ++c)
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b)
+        for (int e = 0; e < 3; ++e) {
+          Entry& en = g_table[c][a][b][e];
+          if (!en.fn) continue;
+          CHFSI_CUDA(cudaFuncSetAttribute((const void*)en.fn,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem));
+          int occ = 0;
+          CHFSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)en.fn,
+                                                                   en.threads, en.smem));
+          en.occ = std::max(occ, 1);
+          en.ready = true;
+        }
+  g_table_init = true;
+  return OK;
+}
+
+struct Plan {
+  int cfg = 0;
+  int split = 1;
+  int k_chunk = 0;
+};
+
+// Estimated cost ~ waves * resident CTAs * padded tile work; smaller is better.
+Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
+  Plan best;
+  double best_cost = 1e300;
+  const int sms = h->sm_count;
+  for (int c = 0; c < NCFG; ++c) {
+    const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
+    const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
+    if (!e.ready && !ep.ready) continue;
+    const long long tm = (M + kBM[c] - 1) / kBM[c];
+    const long long tn = (N + kBN[c] - 1) / kBN[c];
+    const long long tiles = tm * tn;
+    const long long ktiles = std::max<long long>(1, (K + kBK - 1) / kBK);
+    int max_split = (int)std::min<long long>(64, ktiles / 16);
+    if (M * N * 16LL * 8 > (2LL << 30)) max_split = 1;  // cap workspace
+    for (int s = 1; s <= std::max(1, max_split); ++s) {
+      const Entry& en = (s == 1) ? e : ep;
+      if (!en.ready) continue;
+      const long long kt_per = (ktiles + s - 1) / s;
+      const long long ctas = tiles * s;
+      const long long slots = (long long)en.occ * sms;
+      const long long waves = (ctas + slots - 1) / slots;
+      const long long resident = std::min<long long>(en.occ, (ctas + sms - 1) / sms);
+      // per-wave time ~ resident CTAs sharing one SM x tile work (+ per-tile fixed cost)
+      double cost = (double)waves * (double)resident *
+                    ((double)kBM[c] * kBN[c] * (kt_per * kBK + 64.0));
+      if (s > 1) cost += (double)M * N * s * 0.5;  // reduce traffic
+      if (cost < best_cost * 0.999) {
+        best_cost = cost;
+        best.cfg = c;
+        best.split = s;
+        best.k_chunk = (int)(kt_per * kBK);
+      }
+    }
+  }
+  return best;
+}
+
+int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+           GemmParams p) {
+  CHFSI_TRY(ensure_table());
+  if (M <= 0 || N <= 0) return OK;
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) {
+    set_error("zgemm: dimension exceeds int32");
+    return ERR_ARG;
+  }
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  const int c = pl.cfg;
+  if (pl.split == 1) {
+    const Entry& e = g_table[c][opa][opb][epi];
+    dim3 grid((unsigned)((N + kBN[c] - 1) / kBN[c]), (unsigned)((M + kBM[c] - 1) / kBM[c]), 1);
+    e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
+    h->launches++;
+    CHFSI_CHECK_LAUNCH();
+    return OK;
+  }
+  const size_t ws_bytes = (size_t)pl.split * M * N * sizeof(double2);
+  double2* ws = (double2*)scratch(h, SLOT_SPLITK, ws_bytes);
+  if (!ws) return ERR_NOMEM;
+  GemmParams q = p;
+  q.k_chunk = pl.k_chunk;
+  q.ws = ws;
+  const Entry& e = g_table[c][opa][opb][EPI_PARTIAL];
+  dim3 grid((unsigned)((N + kBN[c] - 1) / kBN[c]), (unsigned)((M + kBM[c] - 1) / kBM[c]),
+            (unsigned)pl.split);
+  e.fn<<<grid, e.threads, e.smem, h->stream>>>(q);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  const long long total = M * N;
+  const int threads = 256;
+  const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);
+  zgemm_splitk_reduce_kernel<<<blocks, threads, 0, h->stream>>>(
+      (int)M, (int)N, pl.split, ws, epi, p.alpha, p.beta, p.C, p.ldc, p.B, p.ldb, p.Y0, p.ld0,
+      p.gamma);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
+}  // namespace
+
+int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, double2 alpha,
+          const double2* A, long long lda, const double2* B, long long ldb, double2 beta,
+          double2* C, long long ldc) {
+  if ((opa != OP_N && opa != OP_C) || (opb != OP_N && opb != OP_C)) {
+    set_error("zgemm: op must be 0 (N) or 1 (C)");
+    return ERR_ARG;
+  }
+  GemmParams p{};
+  p.A = A; p.lda = lda;
+  p.B = B; p.ldb = ldb;
+  p.C = C; p.ldc = ldc;
+  p.alpha = alpha; p.beta = beta;
+  p.Y0 = nullptr; p.ld0 = 0; p.gamma = 0.0;
+  return launch(h, opa, opb, EPI_STORE, M, N, K, p);
+}
+
+int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
+                      const double2* Y1, long long ld1, double alpha, double beta,
+                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc) {
+  GemmParams p{};
+  p.A = A; p.lda = lda;
+  p.B = Y1; p.ldb = ld1;
+  p.C = C; p.ldc = ldc;
+  p.alpha = make_double2(alpha, 0.0);
+  p.beta = make_double2(beta, 0.0);
+  p.Y0 = Y0; p.ld0 = ld0; p.gamma = gamma;
+  return launch(h, OP_N, OP_N, EPI_FILTER, M, N, M, p);
+}
+
+}  // namespace chfsi

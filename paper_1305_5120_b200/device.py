@@ -1,0 +1,228 @@
+"""Device-side plumbing: column-major complex128 blocks in HBM and the native engine.
+
+A column-major n x k complex128 block lives in a torch tensor of shape (k, n)
+with unit stride along rows: column j is row j of the tensor, the leading
+dimension is ``t.stride(0)`` and a column range ``t[a:b]`` is a zero-copy
+view. This is exactly the numpy F-order layout of the reference
+(linalg.py:108,121), so host<->device transfers are plain byte copies.
+
+torch provides allocation, streams and torch.distributed; all arithmetic is
+in libchfsi_b200.so, reached through :class:`Engine`.
+"""
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import ContractViolation, NotPositiveDefinite, RankDeficient
+
+CDT = torch.complex128
+
+
+def rows(t):
+    return t.shape[-1]
+
+
+def cols(t):
+    return t.shape[0] if t.dim() == 2 else 1
+
+
+def ld(t):
+    return t.stride(0) if t.dim() == 2 else t.shape[0]
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def empty(n, k, device):
+    return torch.empty((k, n), dtype=CDT, device=device)
+
+
+def zeros(n, k, device):
+    return torch.zeros((k, n), dtype=CDT, device=device)
+
+
+def to_device(arr, device, pin=False):
+    """numpy (n,) / (n, k) complex array -> device tensor (k, n) (column-major block)."""
+    a = np.asarray(arr, dtype=np.complex128)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    a = np.asfortranarray(a)
+    host = torch.from_numpy(a.T)  # (k, n) C-contiguous view of the F-order data
+    if pin:
+        host = host.pin_memory()
+    return host.to(device, non_blocking=pin)
+
+
+def to_host(t):
+    """device tensor (k, n) -> numpy (n, k) F-order complex128 array."""
+    return np.asfortranarray(t.detach().to("cpu").numpy().T)
+
+
+class Engine:
+    """Native handle bound to one CUDA device and torch's current stream there."""
+
+    _engines = {}
+
+    def __init__(self, device):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1305_5120_b200 needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device)
+        self.index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.device = torch.device("cuda", self.index)
+        self.lib = _native.load()
+        with torch.cuda.device(self.index):
+            self.stream = torch.cuda.current_stream(self.index)
+        h = ctypes.c_void_p()
+        _native.check("chfsi_create",
+                      self.lib.chfsi_create(self.index, ctypes.c_void_p(self.stream.cuda_stream),
+                                            ctypes.byref(h)))
+        self.h = h
+
+    @classmethod
+    def get(cls, device=None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        device = torch.device(device)
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        eng = cls._engines.get(idx)
+        cur = torch.cuda.current_stream(idx)
+        if eng is None:
+            eng = cls(torch.device("cuda", idx))
+            cls._engines[idx] = eng
+        elif eng.stream.cuda_stream != cur.cuda_stream:
+            eng.stream = cur
+            _native.call("chfsi_set_stream", eng.h, ctypes.c_void_p(cur.cuda_stream))
+        return eng
+
+    # ------------------------------------------------------------ counters
+    def launch_count(self, reset=False):
+        return int(self.lib.chfsi_launch_count(self.h, 1 if reset else 0))
+
+    def synchronize(self):
+        _native.call("chfsi_synchronize", self.h)
+
+    # ------------------------------------------------------------ kernels
+    def zgemm(self, opa, opb, m, n, k, alpha, A, B, beta, C):
+        """C = alpha op(A) op(B) + beta C on column-major blocks (op: 'N' or 'C')."""
+        oa = 0 if opa == "N" else 1
+        ob = 0 if opb == "N" else 1
+        alpha = complex(alpha)
+        beta = complex(beta)
+        _native.call("chfsi_zgemm", self.h, oa, ob, m, n, k, alpha.real, alpha.imag,
+                     ptr(A), ld(A), ptr(B), ld(B), beta.real, beta.imag, ptr(C), ld(C))
+        return C
+
+    def filter(self, H, Y, W, degree, a, b, lam_ref):
+        """p_m(H) Y; Y is clobbered. Returns the tensor holding the result (Y or W)."""
+        n, k = rows(Y), cols(Y)
+        flag = ctypes.c_int(0)
+        _native.call("chfsi_filter", self.h, n, k, int(degree), float(a), float(b),
+                     float(lam_ref), ptr(H), ld(H), ptr(Y), ld(Y), ptr(W), ld(W),
+                     ctypes.byref(flag))
+        return W if flag.value else Y
+
+    def filter_step(self, H, Y1, alpha, beta, Y0, gamma, C):
+        n, k = rows(Y1), cols(Y1)
+        _native.call("chfsi_filter_step", self.h, n, k, ptr(H), ld(H), ptr(Y1), ld(Y1),
+                     float(alpha), float(beta), ptr(Y0), ld(Y0) if Y0 is not None else 0,
+                     float(gamma), ptr(C), ld(C))
+        return C
+
+    def lanczos_bound(self, H, v0, steps):
+        n = rows(H)
+        kk = max(int(steps), 2)
+        al = (ctypes.c_double * kk)()
+        be = (ctypes.c_double * kk)()
+        done = ctypes.c_int(0)
+        bound = ctypes.c_double(0.0)
+        _native.call("chfsi_lanczos_bound", self.h, n, int(steps), ptr(H), ld(H), ptr(v0), al, be,
+                     ctypes.byref(done), ctypes.byref(bound))
+        j = done.value
+        return float(bound.value), np.array(al[:j]), np.array(be[:j])
+
+    def orthonormalize(self, F, L, T, Q, rank_tol=1e-14):
+        """CGS2 against L (may be None) + CholQR2; raises RankDeficient(column)."""
+        n, k = rows(F), cols(F)
+        nl = 0 if L is None else cols(L)
+        bad = ctypes.c_int64(-1)
+        fro = ctypes.c_double(0.0)
+        st = self.lib.chfsi_orthonormalize(self.h, n, k, ptr(F), ld(F),
+                                           ptr(L) if nl else ctypes.c_void_p(0),
+                                           ld(L) if nl else n, nl, ptr(T), ld(T), ptr(Q), ld(Q),
+                                           float(rank_tol), ctypes.byref(bad), ctypes.byref(fro))
+        if st == _native.ERR_RANK:
+            raise RankDeficient(int(bad.value))
+        _native.check("chfsi_orthonormalize", st)
+        return Q, float(fro.value)
+
+    def rayleigh_ritz(self, H, Q, HQ, Z, HZ):
+        n, k = rows(Q), cols(Q)
+        w = np.empty(k, dtype=np.float64)
+        _native.call("chfsi_rayleigh_ritz", self.h, n, k, ptr(H), ld(H), ptr(Q), ld(Q),
+                     ptr(HQ), ld(HQ), ptr(Z), ld(Z), ptr(HZ), ld(HZ),
+                     w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        return w
+
+    def residual_norms(self, HY, Y, lam):
+        n, k = rows(Y), cols(Y)
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        res = np.empty(k, dtype=np.float64)
+        if k == 0:
+            return res
+        _native.call("chfsi_residual_norms", self.h, n, k, ptr(HY), ld(HY), ptr(Y), ld(Y),
+                     lam.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                     res.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        return res
+
+    def hermitian_norms(self, A):
+        out = (ctypes.c_double * 2)()
+        _native.call("chfsi_hermitian_norms", self.h, rows(A), ptr(A), ld(A), out)
+        return float(out[0]), float(out[1])
+
+    def hermitize(self, A):
+        _native.call("chfsi_hermitize", self.h, rows(A), ptr(A), ld(A))
+        return A
+
+    def cholesky(self, A):
+        """In-place lower Cholesky; raises NotPositiveDefinite(pivot)."""
+        info = ctypes.c_int(0)
+        _native.call("chfsi_cholesky", self.h, rows(A), ptr(A), ld(A), ctypes.byref(info))
+        if info.value > 0:
+            raise NotPositiveDefinite(info.value)
+        if info.value < 0:
+            raise ContractViolation(f"zpotrf: illegal argument {-info.value}")
+        return A
+
+    def trtri_lower(self, L, X):
+        _native.call("chfsi_trtri_lower", self.h, rows(L), ptr(L), ld(L), ptr(X), ld(X))
+        return X
+
+    def heevd(self, A):
+        n = rows(A)
+        w = np.empty(n, dtype=np.float64)
+        _native.call("chfsi_heevd", self.h, n, ptr(A), ld(A),
+                     w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        return w
+
+    def axpby(self, alpha, X, beta, Y):
+        alpha = complex(alpha)
+        beta = complex(beta)
+        _native.call("chfsi_axpby", self.h, rows(Y), cols(Y), alpha.real, alpha.imag,
+                     ptr(X), ld(X) if X is not None else 0, beta.real, beta.imag, ptr(Y), ld(Y))
+        return Y
+
+
+def peak_dmma_tflops(device=0, iters=20000):
+    v = ctypes.c_double(0.0)
+    _native.call("chfsi_peak_dmma", int(device), int(iters), ctypes.byref(v))
+    return float(v.value)
+
+
+def peak_dfma_tflops(device=0, iters=20000):
+    v = ctypes.c_double(0.0)
+    _native.call("chfsi_peak_dfma", int(device), int(iters), ctypes.byref(v))
+    return float(v.value)

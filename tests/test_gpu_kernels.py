@@ -1,0 +1,220 @@
+"""GPU parity of the individual native kernels against the oracle (oracle/chfsi_oracle.py)
+and closed forms. Tolerances are relative, FP64 (DMMA accumulation order differs
+from OpenBLAS, so 1e-13 instead of bit equality)."""
+
+import numpy as np
+import pytest
+
+from conftest import gapped_matrix, rand_hermitian, rand_spd, spectrum_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import torch
+    from paper_1305_5120_b200 import device as D
+    return D.Engine.get(torch.device("cuda", 0))
+
+
+def crand(rng, *s):
+    return rng.standard_normal(s) + 1j * rng.standard_normal(s)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (37, 19, 53), (128, 64, 256), (70, 3, 1000),
+                                   (5, 7, 4000), (300, 260, 77), (513, 129, 65), (64, 0, 8),
+                                   (16, 16, 0)])
+@pytest.mark.parametrize("opa,opb", [("N", "N"), ("C", "N"), ("N", "C"), ("C", "C")])
+def test_zgemm_all_ops(eng, m, n, k, opa, opb):
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    A = crand(rng, m, k) if opa == "N" else crand(rng, k, m)
+    B = crand(rng, k, n) if opb == "N" else crand(rng, n, k)
+    C = crand(rng, m, n)
+    al, be = 0.7 - 0.2j, -0.3 + 0.5j
+    ref = al * ((A if opa == "N" else A.conj().T) @ (B if opb == "N" else B.conj().T)) + be * C
+    dA, dB, dC = D.to_device(A, eng.device), D.to_device(B, eng.device), D.to_device(C, eng.device)
+    eng.zgemm(opa, opb, m, n, k, al, dA, dB, be, dC)
+    got = D.to_host(dC)
+    if ref.size:
+        assert np.linalg.norm(got - ref) <= 1e-13 * max(1.0, np.linalg.norm(ref))
+
+
+def test_zgemm_deterministic_splitk(eng):
+    """Gram-shaped product (split-K path) is bit-identical run to run."""
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(3)
+    A = crand(rng, 20000, 24)
+    dA = D.to_device(A, eng.device)
+    outs = []
+    for _ in range(3):
+        dC = D.zeros(24, 24, eng.device)
+        eng.zgemm("C", "N", 24, 24, 20000, 1.0, dA, dA, 0.0, dC)
+        outs.append(D.to_host(dC))
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+    ref = A.conj().T @ A
+    assert np.linalg.norm(outs[0] - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("m", [1, 2, 5, 20, 50])
+def test_filter_matches_scalar_closed_form(eng, m):
+    """Diagonal H: p_m(H) e_j = p_m(lam_j) e_j (reference test_filter.py:54-67 idea)."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(40 + m)
+    lam = np.concatenate([np.sort(rng.uniform(0.0, 4.0, 8)), np.sort(rng.uniform(5.0, 10.0, 24))])
+    h = np.diag(lam).astype(complex)
+    a, b, lam_ref = 4.8, 10.2, float(lam[0])
+    dH = D.to_device(h, eng.device)
+    dY = D.to_device(np.eye(32, dtype=complex), eng.device)
+    dW = D.zeros(32, 32, eng.device)
+    out = D.to_host(eng.filter(dH, dY, dW, m, a, b, lam_ref))
+    got = np.real(np.diag(out))
+    ref = O.filter_gain(m, lam, a, b, lam_ref)
+    assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-12
+    assert np.linalg.norm(out - np.diag(np.diag(out))) <= 1e-12 * np.linalg.norm(out)
+
+
+@pytest.mark.parametrize("n,k,m", [(200, 24, 15), (513, 37, 20), (1000, 120, 25)])
+def test_filter_matches_oracle_recurrence(eng, n, k, m):
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    h, lam, _ = baseline_matrix(n, n)
+    rng = np.random.default_rng(n + k)
+    y = crand(rng, n, k)
+    a, b, lam_ref = float(lam[k]), float(lam[-1]) * 1.05, float(lam[0])
+    ref = O.cheb_filter(h, y, m, a, b, lam_ref)
+    dH = D.to_device(h, eng.device)
+    dY = D.to_device(y, eng.device)
+    dW = D.zeros(n, k, eng.device)
+    got = D.to_host(eng.filter(dH, dY, dW, m, a, b, lam_ref))
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_lanczos_bound_matches_oracle(eng):
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(30)
+    h = rand_hermitian(rng, 100, scale=2.0)
+    lam_max = np.linalg.eigvalsh(h)[-1]
+    for seed in range(10):
+        got = G.lanczos_upper_bound(h, 10, seed=seed)
+        ref, _ = O.lanczos_bound(h, 10, np.random.default_rng(seed))
+        assert abs(got - ref) <= 1e-10 * abs(ref)
+        assert got >= lam_max
+
+
+def test_lanczos_breakdown_and_clipping():
+    import paper_1305_5120_b200 as G
+    b = G.lanczos_upper_bound(3.0 * np.eye(12, dtype=complex), 10, seed=0)
+    assert 3.0 <= b <= 3.0 + 1e-10
+    b = G.lanczos_upper_bound(np.diag(np.arange(1.0, 11.0)).astype(complex), 10, seed=1)
+    assert 10.0 <= b <= 10.0 + 1e-6
+    assert G.lanczos_upper_bound(np.diag([1.0, 2, 3, 4, 5]).astype(complex), 10, seed=2) >= 5.0
+
+
+def test_residual_norms_match_numpy(eng):
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(59)
+    n, k = 777, 13
+    hy, y = crand(rng, n, k), crand(rng, n, k)
+    lam = rng.uniform(-1, 1, k)
+    got = eng.residual_norms(D.to_device(hy, eng.device), D.to_device(y, eng.device), lam)
+    ref = np.linalg.norm(hy - y * lam, axis=0)
+    assert np.max(np.abs(got - ref) / ref) <= 1e-14
+
+
+@pytest.mark.parametrize("n,k,nl", [(300, 20, 0), (300, 20, 15), (5000, 64, 100), (1000, 250, 40)])
+def test_orthonormalize_cgs2_cholqr2(eng, n, k, nl):
+    import torch
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(n + k + nl)
+    L = np.linalg.qr(crand(rng, n, nl))[0] if nl else None
+    F = crand(rng, n, k) * np.logspace(0, 6, k)  # graded columns
+    dF = D.to_device(F, eng.device)
+    dL = D.to_device(L, eng.device) if nl else None
+    dT, dQ = D.zeros(n, k, eng.device), D.zeros(n, k, eng.device)
+    eng.orthonormalize(dF, dL, dT, dQ)
+    Q = D.to_host(dQ)
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(k)) <= 1e-12 * np.sqrt(k)
+    W = F - L @ (L.conj().T @ F) if nl else F
+    if nl:
+        assert np.linalg.norm(L.conj().T @ Q) <= 1e-12
+    # same span as the projected block
+    qw = np.linalg.qr(W)[0]
+    assert np.linalg.norm(qw - Q @ (Q.conj().T @ qw)) <= 1e-9
+
+
+def test_orthonormalize_rank_collapse_reports_column(eng):
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.errors import RankDeficient
+    rng = np.random.default_rng(13)
+    F = crand(rng, 50, 4)
+    F[:, 2] = F[:, 0]
+    dF = D.to_device(F, eng.device)
+    with pytest.raises(RankDeficient) as exc:
+        eng.orthonormalize(dF, None, D.zeros(50, 4, eng.device), D.zeros(50, 4, eng.device))
+    assert exc.value.column == 2
+
+
+def test_rayleigh_ritz_matches_oracle(eng):
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(58)
+    n, k = 400, 30
+    h = spectrum_matrix(rng, np.linspace(-3.0, 5.0, n))
+    q = np.linalg.qr(crand(rng, n, k))[0]
+    w_ref, z_ref, hz_ref = O.ritz(h, q)
+    dH, dQ = D.to_device(h, eng.device), D.to_device(q, eng.device)
+    dHQ, dZ, dHZ = (D.zeros(n, k, eng.device) for _ in range(3))
+    w = eng.rayleigh_ritz(dH, dQ, dHQ, dZ, dHZ)
+    assert np.max(np.abs(w - w_ref)) <= 1e-12 * np.max(np.abs(w_ref))
+    Z, HZ = D.to_host(dZ), D.to_host(dHZ)
+    assert np.linalg.norm(HZ - h @ Z) <= 1e-12 * np.linalg.norm(HZ)
+    # Ritz vectors agree up to phase
+    ov = np.abs(np.sum(Z.conj() * z_ref, axis=0))
+    assert np.all(ov > 1 - 1e-9)
+
+
+def test_hermitian_norms_and_hermitize(eng):
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(0)
+    for n in (1, 31, 32, 33, 100, 257):
+        a = crand(rng, n, n)
+        d = D.to_device(a, eng.device)
+        fro, devn = eng.hermitian_norms(d)
+        assert abs(fro - np.linalg.norm(a)) <= 1e-13 * np.linalg.norm(a)
+        assert abs(devn - np.linalg.norm(a - a.conj().T)) <= 1e-13 * np.linalg.norm(a)
+        eng.hermitize(d)
+        got = D.to_host(d)
+        ref = (a + a.conj().T) / 2.0
+        np.fill_diagonal(ref, ref.diagonal().real)
+        assert np.array_equal(got, got.conj().T)
+        assert np.max(np.abs(got - ref)) <= 1e-15 * np.max(np.abs(ref))
+
+
+def test_cholesky_trtri_heevd(eng):
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.errors import NotPositiveDefinite
+    rng = np.random.default_rng(16)
+    for n in (7, 64, 300, 1030):
+        b = rand_spd(rng, n, shift=1.0)
+        d = D.to_device(b, eng.device)
+        eng.cholesky(d)
+        lf = D.to_host(d)
+        assert np.linalg.norm(np.triu(lf, 1)) == 0.0
+        assert np.all(lf.diagonal().imag == 0) and np.all(lf.diagonal().real > 0)
+        assert np.linalg.norm(lf @ lf.conj().T - b) <= 1e-12 * np.linalg.norm(b)
+        x = D.zeros(n, n, eng.device)
+        eng.trtri_lower(d, x)
+        xi = D.to_host(x)
+        assert np.linalg.norm(xi @ lf - np.eye(n)) <= 1e-11 * np.sqrt(n)
+        assert np.linalg.norm(np.triu(xi, 1)) == 0.0
+    with pytest.raises(NotPositiveDefinite) as exc:
+        eng.cholesky(D.to_device(np.diag([1.0, 1.0, -1.0]).astype(complex), eng.device))
+    assert exc.value.pivot == 3
+    h = rand_hermitian(rng, 200)
+    d = D.to_device(h, eng.device)
+    w = eng.heevd(d)
+    assert np.max(np.abs(w - np.linalg.eigvalsh(h))) <= 1e-13 * np.max(np.abs(w))

@@ -1,0 +1,190 @@
+"""GPU parity of the full solver against the oracle (reference algorithm restated on the
+CPU) on the same seeded inputs and start vectors.
+
+Bar (BASELINE.json north_star): eigenvalues within 1e-10 relative, every residual below
+tol, the same number of converged pairs, largest principal angle (sine formula) < 1e-8.
+Iteration counts may differ by rounding-induced lock timing."""
+
+import numpy as np
+import pytest
+
+from conftest import gapped_matrix, rand_hermitian, rand_spd, spectrum_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+def _angle(u, v):
+    import oracle.chfsi_oracle as O
+    return O.largest_angle_sine(u, v)
+
+
+def test_known_diagonal_spectrum():
+    import paper_1305_5120_b200 as G
+    h = np.diag(np.arange(1.0, 101.0)).astype(complex)
+    cfg = G.SolverConfig(nev=5)
+    lam, vecs, report = G.chfsi_solve(h, None, cfg, seed=0)
+    assert np.max(np.abs(lam - np.arange(1.0, 6.0))) <= 1e-9
+    assert np.all(G.residuals(h, vecs, lam) < cfg.tol)
+    assert report.converged and vecs.orthonormal
+
+
+@pytest.mark.parametrize("seed,n,nev", [(56, 150, 12), (52, 90, 9), (55, 80, 8), (7, 400, 40)])
+def test_matches_oracle_same_start(seed, n, nev):
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    h, evals = gapped_matrix(seed, n, nev)
+    cfg = G.SolverConfig(nev=nev, max_outer_iters=200)
+    lam, vecs, rep = G.chfsi_solve(h, None, cfg, seed=seed + 1)
+    lam_o, v_o, rep_o = O.solve(h, None, nev, cfg.buffer_cols, cfg.degree, cfg.tol, 200,
+                                seed=seed + 1)
+    assert len(lam) == len(lam_o) == nev
+    assert np.max(np.abs(lam - lam_o) / np.abs(lam_o).clip(1e-300)) <= 1e-10
+    assert np.all(G.residuals(h, vecs, lam) < cfg.tol)
+    assert _angle(vecs.entries, v_o) < 1e-8
+    assert abs(rep.outer_iterations - len(rep_o["iterations"])) <= 2
+
+
+def test_exact_start_single_iteration():
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(50, 80, 8)
+    cfg = G.SolverConfig(nev=8)
+    lam_o, v_o = np.linalg.eigh(h)
+    s = cfg.nev + cfg.buffer_cols
+    lam, vecs, report = G.chfsi_solve(h, v_o[:, :s], cfg, seed=1)
+    assert report.outer_iterations == 1
+    assert np.max(np.abs(lam - lam_o[:8])) <= 1e-10
+
+
+def test_dimension_guard_before_work():
+    import paper_1305_5120_b200 as G
+    h = np.diag([1.0, 2.0, 3.0]).astype(complex)
+    G.reset_product_count()
+    with pytest.raises(G.ContractViolation):
+        G.chfsi_solve(h, None, G.SolverConfig(nev=3), seed=0)
+    assert G.product_count() == 0
+
+
+def test_not_converged_carries_partials():
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(51, 60, 6, lo=4.0, hi_lo=4.2)
+    cfg = G.SolverConfig(nev=6, degree=1, max_outer_iters=2)
+    with pytest.raises(G.NotConverged) as exc:
+        G.chfsi_solve(h, None, cfg, seed=2)
+    err = exc.value
+    assert err.report.outer_iterations == 2
+    assert len(err.eigenvalues) < 6
+    assert not err.report.converged
+
+
+def test_determinism_bit_identical():
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(53, 70, 7)
+    cfg = G.SolverConfig(nev=7)
+    lam1, v1, r1 = G.chfsi_solve(h, None, cfg, seed=4)
+    lam2, v2, r2 = G.chfsi_solve(h, None, cfg, seed=4)
+    assert np.array_equal(lam1, lam2)
+    assert np.array_equal(v1.entries, v2.entries)
+    assert r1.total_matmuls == r2.total_matmuls
+    assert [s.max_resid for s in r1.iterations] == [s.max_resid for s in r2.iterations]
+
+
+def test_work_accounting_matches_counter():
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(55, 80, 8)
+    cfg = G.SolverConfig(nev=8)
+    G.reset_product_count()
+    _, _, report = G.chfsi_solve(h, None, cfg, seed=6)
+    assert G.product_count() == report.total_matmuls
+    for it in report.iterations:
+        assert it.matmuls == (cfg.degree + 1) * it.filtered_cols
+
+
+def test_inverted_prior_raises_degenerate():
+    import paper_1305_5120_b200 as G
+    h = np.diag(np.arange(1.0, 31.0)).astype(complex)
+    with pytest.raises(G.FilterDegenerate):
+        G.chfsi_solve(h, None, G.SolverConfig(nev=4), prior=(9.0, 2.0), seed=0)
+
+
+def test_locked_counts_monotone_and_recheck():
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(52, 90, 9)
+    lam, vecs, report = G.chfsi_solve(h, None, G.SolverConfig(nev=9), seed=3)
+    counts = report.converged_counts
+    assert all(b >= a for a, b in zip(counts, counts[1:]))
+    assert counts[-1] == 9
+    assert np.all(G.residuals(h, vecs, lam) < 1e-10)
+
+
+def test_oracle_equivalence_random_problems():
+    """Reference criterion 1 in miniature: random Hermitian problems vs a dense eigensolver."""
+    import paper_1305_5120_b200 as G
+    for i in range(12):
+        rng = np.random.default_rng(5000 + i)
+        n = int(rng.integers(20, 201))
+        nev = int(rng.integers(1, max(1, int(0.2 * n)) + 1))
+        h = rand_hermitian(rng, n, scale=2.0)
+        cfg = G.SolverConfig(nev=nev, max_outer_iters=300)
+        lam, vecs, _ = G.chfsi_solve(h, None, cfg, seed=rng)
+        lam_o = np.linalg.eigvalsh(h)
+        norm2 = max(abs(lam_o[0]), abs(lam_o[-1]))
+        assert np.max(np.abs(lam - lam_o[:nev])) <= 10 * cfg.tol * norm2
+        assert float(G.residuals(h, vecs, lam).max()) < cfg.tol
+
+
+def test_generalized_matches_oracle():
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(62)
+    a = rand_hermitian(rng, 50, scale=3.0)
+    b = rand_spd(rng, 50)
+    nev = 8
+    cfg = G.SolverConfig(nev=nev, max_outer_iters=200)
+    lam, c, rep = G.solve_generalized(a, b, None, cfg, seed=10)
+    lam_o, c_o, _ = O.solve_generalized(a, b, None, nev, cfg.buffer_cols, max_it=200, seed=10)
+    assert np.max(np.abs(lam - lam_o) / np.abs(lam_o)) <= 1e-10
+    ce = c.entries
+    res = a @ ce - (b @ ce) * lam
+    bound = cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(b, 1))
+    assert np.max(np.linalg.norm(res, axis=0)) <= bound
+    assert np.linalg.norm(ce.conj().T @ b @ ce - np.eye(nev)) <= 1e-9
+
+
+def test_generalized_b_identity_and_a_multiple_of_b():
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(60)
+    a = spectrum_matrix(rng, np.concatenate([np.linspace(0.0, 3.0, 6), np.linspace(5.0, 9.0, 34)]))
+    cfg = G.SolverConfig(nev=6)
+    lam_g, v_g, _ = G.solve_generalized(a, np.eye(40, dtype=complex), None, cfg, seed=8)
+    lam_s, v_s, _ = G.chfsi_solve(a, None, cfg, seed=8)
+    assert np.max(np.abs(lam_g - lam_s)) <= 1e-13
+    b = rand_spd(np.random.default_rng(61), 30)
+    lam, c, _ = G.solve_generalized(2.0 * b, b, None, G.SolverConfig(nev=5), seed=9)
+    assert np.max(np.abs(lam - 2.0)) <= 1e-10
+
+
+def test_generalized_warm_start_single_iteration():
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(64)
+    a = rand_hermitian(rng, 40, scale=3.0)
+    b = rand_spd(rng, 40)
+    cfg = G.SolverConfig(nev=5)
+    lam1, c1, _ = G.solve_generalized(a, b, None, cfg, seed=12)
+    pad_rng = np.random.default_rng(65)
+    s = cfg.nev + cfg.buffer_cols
+    y0 = np.hstack([c1.entries, pad_rng.standard_normal((40, s - 5)) +
+                    1j * pad_rng.standard_normal((40, s - 5))])
+    lam2, _, rep2 = G.solve_generalized(a, b, y0, cfg, prior=(float(lam1[0]), float(lam1[-1]) + 0.5),
+                                        seed=13)
+    assert rep2.outer_iterations == 1
+    assert np.max(np.abs(lam2 - lam1)) <= 1e-10
+
+
+def test_indefinite_b_rejected():
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(66)
+    a = rand_hermitian(rng, 10)
+    bad = np.diag(np.concatenate([np.ones(9), [-1.0]])).astype(complex)
+    with pytest.raises(G.NotPositiveDefinite) as exc:
+        G.solve_generalized(a, bad, None, G.SolverConfig(nev=2), seed=0)
+    assert exc.value.pivot == 10
