@@ -1,0 +1,417 @@
+"""Benchmark of the ChFSI hot path on B200 (BASELINE.json metric: filter FP64 TFLOP/s).
+
+Workload (config.workload): BASELINE config 4's Chebyshev filter call --
+n = 20000, the full search block k = nev + nex = 2200 columns, degree m = 25
+-- on H built with the c0 spectrum recipe (seeded, synthetic: no public
+dataset exists). One step = one filter call p_m(H) Y = m fused DMMA GEMM +
+recurrence launches; algorithmic work 8 n^2 k m FLOP per step. At N > 1
+(torchrun, one process per GPU) the k columns are sharded across ranks (H
+replicated, strong scaling) and each step ends with the NCCL all-gather of
+the filtered block, as the solver needs it for QR and Rayleigh-Ritz.
+
+Also reported: e2e (the same filter through the drop-in Python API
+``chebyshev_filter(H, Y, spec)`` with pinned host H/Y, host<->device copies
+inside the timed region), roofline of the dominant kernel (measured FP64
+tensor-pipe peak), GPU clocks during the timed region, the oracle CPU filter
+on the host cores (cpu_baseline), tail-width throughput and a full c0 solve.
+
+``--impl reference`` times the reference algorithm's CPU filter (the oracle
+restatement, numpy/OpenBLAS on all host cores) on a bounded column sample of
+the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "filter FP64 TFLOP/s (ChFSI Chebyshev filter, n=20000, k=nev+nex=2200, m=25)"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=20000)
+    ap.add_argument("--k", type=int, default=2200)
+    ap.add_argument("--degree", type=int, default=25)
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/tail/solve legs")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def workload_cfg(args, n_gpus):
+    return {
+        "workload": "BASELINE c4 first-iteration Chebyshev filter (standard-form H, c0 spectrum recipe)",
+        "n": args.n, "k": args.k, "degree": args.degree, "nev": 2000, "nex": 200,
+        "parallelism": f"column-shard x{n_gpus} (H replicated)" if n_gpus > 1 else "single GPU",
+        "l2": "inputs larger than L2 (H = 6.4 GB per GPU)",
+        "seed": 0,
+    }
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU legs
+def cpu_filter_rate(n, degree, seconds, seed=0):
+    """Oracle CPU filter (numpy zgemm via OpenBLAS, all cores) on a bounded
+    column sample; returns (TFLOP/s, sample description, cores)."""
+    import oracle.chfsi_oracle as O
+    rng = np.random.default_rng(seed)
+    # the operator's values do not change the zgemm cost: a seeded complex
+    # Gaussian Hermitian stands in for the c4 matrix on the host
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = np.asfortranarray((g + g.conj().T) * (0.5 / np.sqrt(n)))
+    del g
+    ks = 32
+    y = rng.standard_normal((n, ks)) + 1j * rng.standard_normal((n, ks))
+    O.cheb_filter(h, y, 1, 0.5, 3.0, -3.0)  # warm-up (thread pool, page faults)
+    done_flops, t_used, calls = 0.0, 0.0, 0
+    while t_used < seconds and calls < 50:
+        t0 = time.perf_counter()
+        O.cheb_filter(h, y, 2, 0.5, 3.0, -3.0)
+        t_used += time.perf_counter() - t0
+        done_flops += 8.0 * n * n * ks * 2
+        calls += 1
+    cores = os.cpu_count()
+    sample = (f"oracle cheb_filter, n={n}, {ks} of {2200} columns, degree 2 per call, {calls} calls "
+              f"({t_used:.1f} s), numpy/OpenBLAS zgemm on {cores} host threads")
+    return done_flops / t_used / 1e12, sample, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    if rank != 0:
+        return
+    import oracle.chfsi_oracle as O
+    n = args.n
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h = np.asfortranarray((g + g.conj().T) * (0.5 / np.sqrt(n)))
+    del g
+    ks = 32
+    y = rng.standard_normal((n, ks)) + 1j * rng.standard_normal((n, ks))
+    step_flops = 8.0 * n * n * ks * 1
+
+    def step():
+        O.cheb_filter(h, y, 1, 0.5, 3.0, -3.0)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    val = step_flops * args.steps / dt / 1e12
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
+        "data": "synthetic (seeded complex Gaussian Hermitian; c4 shape)",
+        "config": dict(workload_cfg(args, 1), sample_columns=ks),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"one filter degree step (zgemm n={n} x {ks} of 2200 columns + "
+                                   f"recurrence) per step, oracle restatement of core.py:263-284, "
+                                   f"numpy/OpenBLAS on {cores} threads"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200 import workloads as Wl
+    from paper_1305_5120_b200.distributed import ColumnShards
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    eng = D.Engine.get(dev)
+    n, k, m = args.n, args.k, args.degree
+
+    # ---- data: H (c0 spectrum recipe, seeded) replicated on every rank
+    t0 = time.perf_counter()
+    H, lam = Wl.spectrum_matrix_torch(0, n, dev)
+    nev = int(round(k * 2000 / 2200))
+    lam_ref, a_edge = float(lam[0]), float(lam[min(nev, n - 1)])
+    v0 = np.random.default_rng(1).standard_normal(n) + 1j * np.random.default_rng(2).standard_normal(n)
+    v0 /= np.linalg.norm(v0)
+    b_up, _, _ = eng.lanczos_bound(H, D.to_device(v0, dev), 10)
+    t_gen = time.perf_counter() - t0
+
+    shards = ColumnShards(k, world)
+    lo, hi = shards.range(rank)
+    kp = hi - lo
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    Yfull = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
+    Y0 = Yfull[lo:hi].clone()
+    Y = torch.empty_like(Y0)
+    W = torch.empty_like(Y0)
+    gathered = torch.empty((shards.padded * world, n), dtype=torch.complex128, device=dev) if world > 1 else None
+
+    def step():
+        Y.copy_(Y0)
+        out = eng.filter(H, Y, W, m, a_edge, b_up, lam_ref)
+        if world > 1:
+            shards.all_gather(out, gathered)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    sampler = ClockSampler(local_rank)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    eng.launch_count(reset=True)
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    f_events = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        Y.copy_(Y0)
+        a.record(stream)
+        out = eng.filter(H, Y, W, m, a_edge, b_up, lam_ref)
+        b.record(stream)
+        if world > 1:
+            shards.all_gather(out, gathered)
+        f_events.append((a, b))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = eng.launch_count(reset=True)
+    t_total = e0.elapsed_time(e1) * 1e-3
+    t_filter = sum(a.elapsed_time(b) for a, b in f_events) * 1e-3
+    tt = torch.tensor([t_total, t_filter], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_total, t_filter = float(tt[0]), float(tt[1])
+    flops_step = 8.0 * n * n * k * m
+    value = flops_step * args.steps / t_total / 1e12
+    ms_per_step = t_total / args.steps * 1e3
+
+    # roofline of the dominant kernel (the fused filter step): per-launch work / duration
+    launch_flops = 8.0 * n * n * kp
+    avg_launch_s = t_filter / (args.steps * m)
+    achieved = launch_flops / avg_launch_s / 1e12
+
+    if rank != 0:
+        return
+    peaks = measured_fp64_peaks(local_rank)
+    peak = peaks["dmma_tflops"]
+    traffic = committed_traffic()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64 DMMA)",
+        "data": "synthetic (seeded; H = Q diag(lambda) Q^H with the c0 spectrum recipe at n=20000)",
+        "config": workload_cfg(args, world),
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "zgemm_dmma_kernel<64,64,8,32,32,4,N,N,EPI_FILTER>",
+                     "peak_source": "measured on this GPU: DMMA.8x8x4 issue-bound microkernel "
+                                    "(chfsi_peak_dmma), best of 3 x ~0.5 s",
+                     "peaks": peaks},
+        "setup_s": t_gen,
+    }
+    if not args.no_extras:
+        line["e2e"] = e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev)
+        line["tail"] = tail_widths(eng, H, n, dev)
+        del H, Yfull, Y0, Y, W
+        torch.cuda.empty_cache()
+        line["solve_c0"] = solve_c0()
+        rate, sample, cores = cpu_filter_rate(n, m, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
+def measured_fp64_peaks(index):
+    from paper_1305_5120_b200 import device as D
+    dm = max(D.peak_dmma_tflops(index, 400000) for _ in range(3))
+    df = max(D.peak_dfma_tflops(index, 400000) for _ in range(3))
+    nominal = 148 * 1.965e9 * 128 / 1e12
+    return {"dmma_tflops": dm, "dfma_tflops": df, "nominal_fp64_tflops_at_max_clock": nominal}
+
+
+def committed_traffic():
+    """dram bytes per launch from the committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "filter_kernel_ncu.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
+    """Same filter through the public API with pinned host inputs; H2D/D2H inside."""
+    import torch
+
+    import paper_1305_5120_b200 as G
+    n, k, m = args.n, args.k, args.degree
+    h_pin = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    h_pin.copy_(H)
+    y_pin = torch.empty((k, n), dtype=torch.complex128, pin_memory=True)
+    y_pin.copy_(Yfull)
+    h_np = h_pin.numpy().T  # F-order n x n view of the pinned buffer (column j = row j)
+    y_np = y_pin.numpy().T
+    spec = G.FilterSpec(degree=m, a=a_edge, b=b_up, lam_ref=lam_ref)
+    out = G.chebyshev_filter(h_np, y_np, spec)  # warm-up
+    _ = out.entries
+    del out
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        out = G.chebyshev_filter(h_np, y_np, spec)
+        res = out.entries  # device -> host of the filtered block
+        del out
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    flops = 8.0 * n * n * k * m
+    return {"value": flops * steps / dt / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": int(16 * n * n + 16 * n * k),
+            "d2h_bytes_per_step": int(res.nbytes), "steps": steps,
+            "path": "paper_1305_5120_b200.chebyshev_filter(H, Y, FilterSpec) -> VectorBlock.entries"}
+
+
+def tail_widths(eng, H, n, dev):
+    """Filter-step throughput at the solve's dominant narrow widths."""
+    import torch
+    out = {}
+    for k in (26, 210, 275):
+        Y1 = torch.randn((k, n), dtype=torch.complex128, device=dev)
+        Y0 = torch.randn((k, n), dtype=torch.complex128, device=dev)
+        for _ in range(2):
+            eng.filter_step(H, Y1, 0.5, -0.1, Y0, 0.2, Y0)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            eng.filter_step(H, Y1, 0.5, -0.1, Y0, 0.2, Y0)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 5
+        out[str(k)] = {"ms": ms, "tflops": 8.0 * n * n * k / (ms * 1e-3) / 1e12}
+    return out
+
+
+def solve_c0():
+    """s per ChFSI solve at BASELINE config 0 (n=1000, nev=100, nex=20, m=15, random start),
+    reference interval semantics; the reference CPU needed 2524 iterations / ~60 s."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    h, lam_true, _ = baseline_matrix(0, 1000)
+    cfg = G.SolverConfig(nev=100, buffer=20, degree=15, max_outer_iters=20000)
+    t0 = time.perf_counter()
+    lam, vecs, rep = G.chfsi_solve(h, None, cfg, seed=1)
+    dt = time.perf_counter() - t0
+    return {"s_per_solve": dt, "outer_iterations": rep.outer_iterations,
+            "max_rel_eig_err_vs_exact": float(np.max(np.abs(lam - lam_true[:100]) / np.abs(lam_true[:100]))),
+            "filter_tflops": rep.filter_tflops, "t_filter": rep.t_filter, "t_qr": rep.t_qr,
+            "t_rr": rep.t_rr, "t_resid": rep.t_resid}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
