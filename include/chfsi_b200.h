@@ -119,6 +119,12 @@ int chfsi_axpby(chfsi_handle_t h, int64_t n, int64_t k, double alpha_re, double 
                 const void* d_X, int64_t ldx, double beta_re, double beta_im, void* d_Y,
                 int64_t ldy);
 
+/* Tuning hooks (process-wide): force GEMM tile config `cfg` (-1 = cost model) and
+ * split-K factor (0 = automatic); query the plan the cost model picks for a shape. */
+int chfsi_gemm_override(int cfg, int split);
+int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m,
+                    int64_t n, int64_t k, int* h_cfg, int* h_split);
+
 /* Microbenchmarks that give the roofline denominators on the box:
  * FP64 tensor-pipe (DMMA) and FP64 FMA-pipe (DFMA) peak, TFLOP/s. */
 int chfsi_peak_dmma(int device, int iters, double* h_tflops);

@@ -70,19 +70,29 @@ int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long lo
                   long long ldz, double2* HZ, long long ldhz, double* w_dev);
 
 // ---------------------------------------------------------------- peaks
+// Register-resident 4 x 4 block of independent 8x8 accumulators fed by 4 A and
+// 4 B fragments, the same operand reuse as a GEMM warp tile (16 DMMA/iteration).
 __global__ void peak_dmma_kernel(int iters, double* out) {
-  constexpr int U = 16;
-  double acc[U][2];
+  double acc[4][4][2];
+  double a[4], b[4];
   #pragma unroll
-  for (int u = 0; u < U; ++u) acc[u][0] = acc[u][1] = 1e-3 * (threadIdx.x + u);
-  const double a = 1.0 + 1e-9 * threadIdx.x, b = 1.0 - 1e-9 * threadIdx.x;
+  for (int i = 0; i < 4; ++i) {
+    a[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+    b[i] = 1.0 - 1e-9 * (threadIdx.x + 3 * i);
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 1e-3 * (i + 4 * j);
+  }
   for (int it = 0; it < iters; ++it) {
     #pragma unroll
-    for (int u = 0; u < U; ++u) dmma884(acc[u][0], acc[u][1], a, b);
+    for (int i = 0; i < 4; ++i)
+      #pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
   }
   double s = 0.0;
   #pragma unroll
-  for (int u = 0; u < U; ++u) s += acc[u][0] + acc[u][1];
+  for (int i = 0; i < 4; ++i)
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) s += acc[i][j][0] + acc[i][j][1];
   if (s == 123.456) out[0] = s;  // defeat dead-code elimination
 }
 
@@ -345,6 +355,14 @@ int chfsi_axpby(chfsi_handle_t h, int64_t n, int64_t k, double alpha_re, double 
   H_CHECK(h);
   return zaxpby_cols(h, n, k, c2(alpha_re, alpha_im), (const double2*)d_X, ldx,
                      c2(beta_re, beta_im), (double2*)d_Y, ldy);
+}
+
+int chfsi_gemm_override(int cfg, int split) { return gemm_override(cfg, split); }
+
+int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m, int64_t n,
+                    int64_t k, int* h_cfg, int* h_split) {
+  H_CHECK(h);
+  return gemm_plan(h, opa, opb, filter_epilogue ? 1 : 0, m, n, k, h_cfg, h_split);
 }
 
 int chfsi_peak_dmma(int device, int iters, double* h_tflops) {

@@ -87,6 +87,11 @@ int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, lon
                       const double2* Y1, long long ld1, double alpha, double beta,
                       const double2* Y0, long long ld0, double gamma, double2* C, long long ldc);
 
+// Tuning hooks: force a tile config (-1 = cost model) / split-K factor (0 = auto).
+int gemm_override(int cfg, int split);
+int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+              int* cfg, int* split);
+
 // ---- misc kernels (kernels.cu) ----
 int residual_norms(Handle* h, long long n, long long k, const double2* HY, long long ldhy,
                    const double2* Y, long long ldy, const double* lam_dev, double* res_dev);

@@ -8,6 +8,7 @@
 // are bit-identical run to run (reference criterion 7, test_acceptance.py:199).
 #include <algorithm>
 #include <cmath>
+#include <string>
 
 #include "internal.h"
 #include "zgemm.cuh"
@@ -72,15 +73,25 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 4;
-// cfg 0: 64x64 (warp 32x32); cfg 1: 64x32 (32x16); cfg 2: 64x16 (16x16); cfg 3: 32x16 (16x8)
+constexpr int NCFG = 7;
+// cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
+// cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
+// cfg 2: 64x16   BK8  warp 16x16 (4 warps)     cfg 6: 128x32 BK8  warp 32x16 (8 warps)
+// cfg 3: 32x16   BK8  warp 16x8  (4 warps)
 using C0 = CfgT<64, 64, 8, 32, 32, 4>;
 using C1 = CfgT<64, 32, 8, 32, 16, 4>;
 using C2 = CfgT<64, 16, 8, 16, 16, 4>;
 using C3 = CfgT<32, 16, 8, 16, 8, 4>;
-const int kBM[NCFG] = {64, 64, 64, 32};
-const int kBN[NCFG] = {64, 32, 16, 16};
-const int kBK = 8;
+using C4 = CfgT<64, 64, 16, 32, 32, 3>;
+using C5 = CfgT<128, 64, 8, 32, 32, 4>;
+using C6 = CfgT<128, 32, 8, 32, 16, 4>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8};
+// relative per-tile throughput (measured on B200, see profiles/); bigger warp tiles
+// amortise fragment loads and barriers
+double g_eff[NCFG] = {0.98, 1.00, 0.96, 0.90, 0.96, 0.90, 0.975};
+int g_force_cfg = -1, g_force_split = 0;
 
 struct Entry {
   KFn fn = nullptr;
@@ -112,6 +123,9 @@ int ensure_table() {
   put_all<C1>(1);
   put_all<C2>(2);
   put_all<C3>(3);
+  put_all<C4>(4);
+  put_all<C5>(5);
+  put_all<C6>(6);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -142,16 +156,20 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   double best_cost = 1e300;
   const int sms = h->sm_count;
   for (int c = 0; c < NCFG; ++c) {
+    if (g_force_cfg >= 0 && c != g_force_cfg) continue;
     const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
     if (!e.ready && !ep.ready) continue;
+    const int bk = kBKc[c];
     const long long tm = (M + kBM[c] - 1) / kBM[c];
     const long long tn = (N + kBN[c] - 1) / kBN[c];
     const long long tiles = tm * tn;
-    const long long ktiles = std::max<long long>(1, (K + kBK - 1) / kBK);
-    int max_split = (int)std::min<long long>(64, ktiles / 16);
+    const long long ktiles = std::max<long long>(1, (K + bk - 1) / bk);
+    int max_split = (int)std::min<long long>(64, ktiles / (128 / bk));
     if (M * N * 16LL * 8 > (2LL << 30)) max_split = 1;  // cap workspace
-    for (int s = 1; s <= std::max(1, max_split); ++s) {
+    int s_lo = 1, s_hi = std::max(1, max_split);
+    if (g_force_split > 0) s_lo = s_hi = g_force_split;
+    for (int s = s_lo; s <= s_hi; ++s) {
       const Entry& en = (s == 1) ? e : ep;
       if (!en.ready) continue;
       const long long kt_per = (ktiles + s - 1) / s;
@@ -159,15 +177,15 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
       const long long slots = (long long)en.occ * sms;
       const long long waves = (ctas + slots - 1) / slots;
       const long long resident = std::min<long long>(en.occ, (ctas + sms - 1) / sms);
-      // per-wave time ~ resident CTAs sharing one SM x tile work (+ per-tile fixed cost)
+      // per-wave time ~ resident CTAs sharing one SM x padded tile work / tile efficiency
       double cost = (double)waves * (double)resident *
-                    ((double)kBM[c] * kBN[c] * (kt_per * kBK + 64.0));
+                    ((double)kBM[c] * kBN[c] * (kt_per * bk + 64.0)) / g_eff[c];
       if (s > 1) cost += (double)M * N * s * 0.5;  // reduce traffic
       if (cost < best_cost * 0.999) {
         best_cost = cost;
         best.cfg = c;
         best.split = s;
-        best.k_chunk = (int)(kt_per * kBK);
+        best.k_chunk = (int)(kt_per * bk);
       }
     }
   }
@@ -187,9 +205,16 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.K = (int)K;
   const Plan pl = choose(h, opa, opb, epi, M, N, K);
   const int c = pl.cfg;
+  p.tiles_m = (int)((M + kBM[c] - 1) / kBM[c]);
+  p.tiles_n = (int)((N + kBN[c] - 1) / kBN[c]);
+  // Row-major raster (consecutive CTAs share one H row strip). A grouped raster
+  // (several row tiles per wave sharing Y strips) measured 1.5 % slower on B200
+  // (profiles/r01), so group = 1.
+  p.group = 1;
+  const unsigned ntiles = (unsigned)((long long)p.tiles_m * p.tiles_n);
   if (pl.split == 1) {
     const Entry& e = g_table[c][opa][opb][epi];
-    dim3 grid((unsigned)((N + kBN[c] - 1) / kBN[c]), (unsigned)((M + kBM[c] - 1) / kBM[c]), 1);
+    dim3 grid(ntiles, 1, 1);
     e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
     h->launches++;
     CHFSI_CHECK_LAUNCH();
@@ -202,8 +227,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   q.k_chunk = pl.k_chunk;
   q.ws = ws;
   const Entry& e = g_table[c][opa][opb][EPI_PARTIAL];
-  dim3 grid((unsigned)((N + kBN[c] - 1) / kBN[c]), (unsigned)((M + kBM[c] - 1) / kBM[c]),
-            (unsigned)pl.split);
+  dim3 grid(ntiles, 1, (unsigned)pl.split);
   e.fn<<<grid, e.threads, e.smem, h->stream>>>(q);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
@@ -219,6 +243,25 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
 }
 
 }  // namespace
+
+int gemm_override(int cfg, int split) {
+  if (cfg >= NCFG || split < 0 || split > 64) {
+    set_error("gemm_override: cfg must be < " + std::to_string(NCFG) + " and split in [0, 64]");
+    return ERR_ARG;
+  }
+  g_force_cfg = cfg;
+  g_force_split = split;
+  return OK;
+}
+
+int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+              int* cfg, int* split) {
+  CHFSI_TRY(ensure_table());
+  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  *cfg = pl.cfg;
+  *split = pl.split;
+  return OK;
+}
 
 int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, double2 alpha,
           const double2* A, long long lda, const double2* B, long long ldb, double2 beta,

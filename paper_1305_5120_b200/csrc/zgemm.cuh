@@ -37,7 +37,21 @@ struct GemmParams {
   // EPI_PARTIAL: K range per blockIdx.z and the [z][N][M] workspace
   int k_chunk;
   double2* ws;
+  // grouped raster: blockIdx.x enumerates tiles so that `group` consecutive row tiles
+  // share each column tile inside one wave (Y strips are reused from L2)
+  int tiles_m, tiles_n, group;
 };
+
+// linear tile id -> (row tile, column tile), grouped raster
+__device__ __forceinline__ void tile_coords(const GemmParams& p, int b, int& mi, int& ni) {
+  const int per_group = p.group * p.tiles_n;
+  const int g = b / per_group;
+  const int first = g * p.group;
+  const int gsize = min(p.tiles_m - first, p.group);
+  const int r = b - g * per_group;
+  mi = first + r % gsize;
+  ni = r / gsize;
+}
 
 template <int BM, int BK, int OPA>
 struct ATile {
@@ -71,7 +85,9 @@ zgemm_dmma_kernel(const GemmParams p) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp % NWM, wn = warp / NWM;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  int mi, ni;
+  tile_coords(p, blockIdx.x, mi, ni);
+  const int m0 = mi * BM, n0 = ni * BN;
   int kbeg = 0, kend = p.K;
   if (EPI == EPI_PARTIAL) {
     kbeg = blockIdx.z * p.k_chunk;
