@@ -345,18 +345,28 @@ class _Workspace:
 class DeviceSolver:
     """One ChFSI solve on a device-resident H (core.py:385-546)."""
 
-    def __init__(self, hm, config, device=None):
+    def __init__(self, hm, config, device=None, group=None):
         self.hm = hm
         self.cfg = config
         self.hb = hm.device_block(device)
         self.device = self.hb.device
         self.eng = engine(self.device)
         self.n = hm.n
+        self.sharded = None
+        if group is not None:
+            from .distributed import ShardedFilter, world_info
+            if world_info(group)[1] > 1:
+                self.sharded = ShardedFilter(group)
 
     # -- phases -------------------------------------------------------
     def _filter(self, active, out_other, a_edge, b_up, lam_ref):
         """Filter the active block in place (active is clobbered); returns the
-        tensor with p_m(H) active: either ``active`` or ``out_other``."""
+        tensor with p_m(H) active: either ``active`` or ``out_other``. With a
+        process group, each rank filters its column shard and the shards are
+        all-gathered (distributed.ShardedFilter)."""
+        if self.sharded is not None:
+            return self.sharded(self.eng, self.hb, active, out_other, self.cfg.degree, a_edge,
+                                b_up, lam_ref)
         return self.eng.filter(self.hb, active, out_other, self.cfg.degree, a_edge, b_up, lam_ref)
 
     def _orthonormalize(self, f, locked, t, q, rng):
@@ -501,11 +511,13 @@ class DeviceSolver:
         return vals, VectorBlock(out, orthonormal=True), report
 
 
-def chfsi_solve(H, Y0, config, prior=None, seed=0):
+def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None):
     """Run ChFSI on a standard Hermitian problem (core.py:385-546).
 
     Same signature, return types, report fields, RNG order and exceptions
-    as the reference; arithmetic on the GPU.
+    as the reference; arithmetic on the GPU. ``group`` (keyword-only, B200
+    extension): a torch.distributed process group with one process per GPU;
+    the filter columns are then sharded across its ranks (H replicated).
     """
     config = _as_config(config)
     if isinstance(H, HermitianDenseMatrix):
@@ -533,10 +545,10 @@ def chfsi_solve(H, Y0, config, prior=None, seed=0):
             raise ContractViolation(f"start block must be {n} x {s_tot}, got {y.shape}")
         y0 = y
     hm = _hermitian(H)
-    return DeviceSolver(hm, config).run(y0, prior, rng)
+    return DeviceSolver(hm, config, group=group).run(y0, prior, rng)
 
 
-def solve_generalized(A, B, Y0, config, prior=None, seed=0):
+def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None):
     """A c = lambda B c for the nev lowest pairs (core.py:549-569):
     B = L L^H (cuSOLVER zpotrf), H = L^-1 A L^-H (triangular inverse + DMMA
     GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors."""
@@ -564,7 +576,7 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0):
         fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
         eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd)
         y0 = VectorBlock(fwd)
-    lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed)
+    lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed, group=group)
     c = dev.empty(n, yv.s, d)
     eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c)
     return lam, VectorBlock(c), report

@@ -40,7 +40,8 @@ class ColumnShards:
         """All-gather (width_r, n) shards into ``gathered`` (padded * world, n).
 
         Column-major blocks are (cols, rows) tensors, so a shard is a contiguous
-        row range and the gather is one flat all_gather_into_tensor."""
+        row range and the gather is one flat all_gather_into_tensor (NCCL over
+        NVLink on B200). Under gloo, device tensors are staged through the host."""
         if self.world == 1:
             gathered[: local.shape[0]].copy_(local)
             return gathered
@@ -53,7 +54,12 @@ class ColumnShards:
         else:
             send = torch.zeros((self.padded, local.shape[1]), dtype=local.dtype, device=local.device)
             send[:w].copy_(local)
-        dist.all_gather_into_tensor(gathered, send, group=group)
+        if _needs_host_staging(send, group):
+            recv = torch.empty(gathered.shape, dtype=gathered.dtype)
+            dist.all_gather_into_tensor(recv, send.cpu(), group=group)
+            gathered.copy_(recv)
+        else:
+            dist.all_gather_into_tensor(gathered, send, group=group)
         return gathered
 
     def compact(self, gathered, out):
@@ -72,18 +78,64 @@ class ColumnShards:
         return self.compact(g, out)
 
 
+def _needs_host_staging(t, group):
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def world_info(group=None):
+    """(rank, world) of ``group``; (0, 1) when torch.distributed is not initialised."""
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
 def all_gather_values(vals, shards, group=None):
     """Gather per-rank 1-D float64 vectors (e.g. residual norms of own columns)."""
     if shards.world == 1:
         return vals
     rank = dist.get_rank(group)
     w = shards.widths[rank]
-    send = torch.zeros(shards.padded, dtype=torch.float64, device=vals.device)
+    stage = _needs_host_staging(vals, group)
+    dev = torch.device("cpu") if stage else vals.device
+    send = torch.zeros(shards.padded, dtype=torch.float64, device=dev)
     send[:w].copy_(vals[:w])
-    recv = torch.empty(shards.padded * shards.world, dtype=torch.float64, device=vals.device)
+    recv = torch.empty(shards.padded * shards.world, dtype=torch.float64, device=dev)
     dist.all_gather_into_tensor(recv, send, group=group)
     out = torch.empty(shards.k, dtype=torch.float64, device=vals.device)
     for r in range(shards.world):
         lo, hi = shards.range(r)
         out[lo:hi].copy_(recv[r * shards.padded: r * shards.padded + hi - lo])
     return out
+
+
+class ShardedFilter:
+    """Column-sharded Chebyshev filter for DeviceSolver.
+
+    Each rank filters its contiguous column range of the active block (no
+    communication inside the filter: core.py:276-283 is column-separable),
+    then the shards are all-gathered so every rank holds the full filtered
+    block for CGS2/CholQR2 and Rayleigh-Ritz. Those later phases run
+    redundantly on identical inputs with deterministic kernels, so every rank
+    reaches the same Ritz values, residuals and locking decision without any
+    further collective.
+    """
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank, self.world = world_info(group)
+        self._buf = None
+
+    def __call__(self, eng, H, active, other, degree, a, b, lam_ref):
+        k, n = active.shape[0], active.shape[1]
+        sh = ColumnShards(k, self.world)
+        lo, hi = sh.range(self.rank)
+        if hi > lo:
+            mine = eng.filter(H, active[lo:hi], other[lo:hi], degree, a, b, lam_ref)
+        else:
+            mine = active[lo:hi]
+        need = sh.padded * self.world
+        if self._buf is None or self._buf.shape[0] < need or self._buf.shape[1] != n:
+            self._buf = torch.empty((need, n), dtype=active.dtype, device=active.device)
+        gathered = self._buf[:need]
+        sh.all_gather(mine, gathered, self.group)
+        return sh.compact(gathered, other[:k])

@@ -188,3 +188,109 @@ def test_indefinite_b_rejected():
     with pytest.raises(G.NotPositiveDefinite) as exc:
         G.solve_generalized(a, bad, None, G.SolverConfig(nev=2), seed=0)
     assert exc.value.pivot == 10
+
+
+# ----------------------------------------------------------------------
+# parity against fixtures produced by the reference itself (tests/golden)
+
+def _gold(name):
+    import os
+    return np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name))
+
+
+@pytest.mark.parametrize("gs,n,nev,ss", [(56, 150, 12, 7), (52, 90, 9, 3), (55, 80, 8, 6),
+                                          (53, 70, 7, 4)])
+def test_small_problems_match_reference_golden(gs, n, nev, ss):
+    import paper_1305_5120_b200 as G
+    g = _gold("solver_small.npz")
+    key = f"g{gs}_n{n}_nev{nev}_s{ss}"
+    h, _ = gapped_matrix(gs, n, nev)
+    lam, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=nev), seed=ss)
+    ref = g[key + "_lam"]
+    assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-10
+    assert _angle(v.entries, g[key + "_v"]) < 1e-8
+    assert len(lam) == len(ref)
+    assert abs(rep.outer_iterations - len(g[key + "_it_converged"])) <= 2
+
+
+def test_baseline_c0_matches_reference_golden():
+    """BASELINE config 0 in full (n=1000, nev=100, nex=20, m=15, tol 1e-10, random
+    start; generator seed 0, solver seed 1) against the reference's own result."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    g = _gold("c0.npz")
+    h, lam_true, _ = baseline_matrix(0, 1000)
+    cfg = G.SolverConfig(nev=100, buffer=20, degree=15, max_outer_iters=20000)
+    lam, v, rep = G.chfsi_solve(h, None, cfg, seed=1)
+    ref = g["lam"]
+    assert len(lam) == len(ref) == 100
+    assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-10
+    assert np.max(G.residuals(h, v, lam)) < cfg.tol
+    assert _angle(v.entries, g["v"]) < 1e-8
+    # iteration trace: the reference needed len(it_converged) iterations
+    n_ref = len(g["it_converged"])
+    assert abs(rep.outer_iterations - n_ref) <= max(5, n_ref // 50)
+
+
+def test_reuse_sequence_matches_reference_golden():
+    """BASELINE c1 recipe at n=200 (3 problems, reuse), driven like the reference's
+    solve_sequence (same pad / solver Generator seeds)."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    g = _gold("sequence_small.npz")
+    probs = baseline_sequence(5, 200, 3)
+    spec = G.SequenceSpec(n=200, N=3, nev=20, seed=5)
+    seq = G.ProblemSequence(spec=spec, problems=[(G.HermitianDenseMatrix(a, rtol=1e-10), None)
+                                                 for a, _ in probs])
+    cfg = G.SolverConfig(nev=20, buffer=4, degree=20, max_outer_iters=5000)
+    rep = G.solve_sequence(seq, cfg, "reuse")
+    for i in range(3):
+        ref = g[f"lam{i}"]
+        assert np.max(np.abs(rep.eigenvalues[i] - ref) / np.abs(ref)) <= 1e-10
+        assert _angle(rep.vectors[i].entries, g[f"v{i}"]) < 1e-8
+        assert abs(rep.reports[i].outer_iterations - int(g[f"iters{i}"])) <= 3
+
+
+def test_generalized_matches_reference_golden():
+    import paper_1305_5120_b200 as G
+    g = _gold("generalized.npz")
+    lam, c, rep = G.solve_generalized(g["a"], g["b"], None, G.SolverConfig(nev=8), seed=10)
+    assert np.max(np.abs(lam - g["lam"]) / np.abs(g["lam"])) <= 1e-10
+    b = g["b"]
+    ce = c.entries
+    assert np.linalg.norm(ce.conj().T @ b @ ce - np.eye(8)) <= 1e-9
+    assert _angle(ce, g["c"]) < 1e-8
+
+
+def test_filter_and_lanczos_match_reference_golden():
+    import paper_1305_5120_b200 as G
+    g = _gold("filter.npz")
+    deg, a, b, lr = g["rand_spec"]
+    out = G.chebyshev_filter(g["rand_h"], g["rand_y"], G.FilterSpec(int(deg), a, b, lr)).entries
+    ref = g["rand_out"]
+    assert np.linalg.norm(out - ref) <= 1e-13 * np.linalg.norm(ref)
+    gl = _gold("lanczos.npz")
+    for s, bref in enumerate(gl["bounds"]):
+        assert abs(G.lanczos_upper_bound(gl["h"], 10, seed=s) - bref) <= 1e-12 * abs(bref)
+
+
+def test_generalized_baseline_recipe_sequence():
+    """c2-style generalized reuse sequence (S = I + 0.1 B^H B/||B^H B||) at n=400:
+    every cycle converges, B-orthonormal, generalized residual below the scaled bound,
+    and eigenvalues agree with the oracle's explicit reduction."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    probs = baseline_sequence(8, 400, 3, generalized=True)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=400, N=3, nev=40, seed=8),
+                            problems=[(a, s) for a, s in probs])
+    cfg = G.SolverConfig(nev=40, buffer=4, degree=20, max_outer_iters=20000)
+    rep = G.solve_sequence(seq, cfg, "reuse")
+    for (a, s), lam, c in zip(probs, rep.eigenvalues, rep.vectors):
+        ce = c.entries
+        res = np.linalg.norm(a @ ce - (s @ ce) * lam, axis=0)
+        assert np.max(res) <= cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(s, 1))
+        assert np.linalg.norm(ce.conj().T @ s @ ce - np.eye(40)) <= 1e-9
+        lf = O.cholesky(s)
+        ref = np.linalg.eigvalsh(O.reduce_standard(a, lf))[:40]
+        assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-10
