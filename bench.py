@@ -273,6 +273,7 @@ def run_b200(args, rank, world, local_rank):
     avg_launch_s = t_filter / (args.steps * m)
     achieved = launch_flops / avg_launch_s / 1e12
 
+    kernel_name = plan_kernel_name(eng, n, kp)
     if rank != 0:
         return
     peaks = measured_fp64_peaks(local_rank)
@@ -288,7 +289,7 @@ def run_b200(args, rank, world, local_rank):
         "clocks": clocks,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "zgemm_dmma_kernel<64,64,8,32,32,4,N,N,EPI_FILTER>",
+                     "kernel": kernel_name,
                      "peak_source": "measured on this GPU: DMMA.8x8x4 issue-bound microkernel "
                                     "(chfsi_peak_dmma), best of 3 x ~0.5 s",
                      "peaks": peaks},
@@ -300,10 +301,62 @@ def run_b200(args, rank, world, local_rank):
         del H, Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         line["solve_c0"] = solve_c0()
+        line["c4_outer_iteration"] = c4_iteration_window()
+        torch.cuda.empty_cache()
         rate, sample, cores = cpu_filter_rate(n, m, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
+
+
+KERNELS = {
+    0: "zgemm_dmma_kernel<64,64,BK8,warp32x32,cp.async x4>",
+    1: "zgemm_dmma_kernel<64,32,BK8,warp32x16,cp.async x4>",
+    2: "zgemm_dmma_kernel<64,16,BK8,warp16x16,cp.async x4>",
+    3: "zgemm_dmma_kernel<32,16,BK8,warp16x8,cp.async x4>",
+    4: "zgemm_dmma_kernel<64,64,BK16,warp32x32,cp.async x3>",
+    5: "zgemm_dmma_kernel<128,64,BK8,warp32x32,cp.async x4>",
+    6: "zgemm_dmma_kernel<128,32,BK8,warp32x16,cp.async x4>",
+    7: "zgemm_tma_kernel<64,32,warp32x16,TMA+mbarrier x4,EPI_FILTER>",
+    8: "zgemm_tma_kernel<64,16,warp16x16,TMA+mbarrier x4,EPI_FILTER>",
+    9: "zgemm_tma_kernel<64,64,warp32x32,TMA+mbarrier x4,EPI_FILTER>",
+}
+
+
+def plan_kernel_name(eng, n, k):
+    import ctypes
+    from paper_1305_5120_b200 import _native
+    cfg, split = ctypes.c_int(), ctypes.c_int()
+    _native.call("chfsi_gemm_plan", eng.h, 0, 0, 1, n, k, n, ctypes.byref(cfg), ctypes.byref(split))
+    name = KERNELS.get(cfg.value, f"cfg{cfg.value}")
+    return name + (f" split-K {split.value}" if split.value > 1 else "")
+
+
+def c4_iteration_window(n=20000, nev=2000, nex=200, degree=25):
+    """One full-width ChFSI outer iteration at c4 shape (bootstrap RR + iteration 1),
+    phase times from the solver's own report (max_outer_iters=1 -> NotConverged)."""
+    import paper_1305_5120_b200 as G
+    import torch
+    from paper_1305_5120_b200 import workloads as Wl
+    H, lam = Wl.spectrum_matrix_torch(0, n, torch.device("cuda", torch.cuda.current_device()))
+    hm = G.HermitianDenseMatrix.from_device(H, trusted=True)
+    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=degree, max_outer_iters=1)
+    t0 = time.perf_counter()
+    try:
+        G.chfsi_solve(hm, None, cfg, seed=1)
+        rep = None
+    except G.NotConverged as exc:
+        rep = exc.report
+    dt = time.perf_counter() - t0
+    if rep is None:
+        return {"error": "converged in one iteration (unexpected)"}
+    it = rep.iterations[0]
+    return {"n": n, "k": nev + nex, "degree": degree, "wall_s": dt,
+            "t_lanczos": rep.t_lanczos, "t_bootstrap_rr": rep.t_rr - it.t_rr,
+            "iteration": {"t_filter": it.t_filter, "t_qr": it.t_qr, "t_rr": it.t_rr,
+                          "t_resid": it.t_resid, "filtered_cols": it.filtered_cols,
+                          "locked": it.converged},
+            "filter_share_of_iteration": it.t_filter / (it.t_filter + it.t_qr + it.t_rr + it.t_resid)}
 
 
 def measured_fp64_peaks(index):

@@ -12,6 +12,9 @@
 
 #include "internal.h"
 #include "zgemm.cuh"
+#include "zgemm_tma.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace chfsi {
 
@@ -73,7 +76,8 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 7;
+constexpr int NCFG = 10;
+constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
 // cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
 // cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
 // cfg 2: 64x16   BK8  warp 16x16 (4 warps)     cfg 6: 128x32 BK8  warp 32x16 (8 warps)
@@ -85,18 +89,32 @@ using C3 = CfgT<32, 16, 8, 16, 8, 4>;
 using C4 = CfgT<64, 64, 16, 32, 32, 3>;
 using C5 = CfgT<128, 64, 8, 32, 32, 4>;
 using C6 = CfgT<128, 32, 8, 32, 16, 4>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8};
+// cfg 7: TMA 64x32 warp 32x16, 4 stages; cfg 8: TMA 64x16 warp 16x16; cfg 9: TMA 64x64 warp 32x32
+using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmParams);
+template <int BM, int BN, int WM, int WN, int ST>
+struct TmaT {
+  static constexpr int threads = (BM / WM) * (BN / WN) * 32;
+  static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST>(); }
+  template <int EPI>
+  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI>; }
+};
+using T7 = TmaT<64, 32, 32, 16, 4>;
+using T8 = TmaT<64, 16, 16, 16, 4>;
+using T9 = TmaT<64, 64, 32, 32, 4>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8};
 // relative per-tile throughput (measured on B200, see profiles/); bigger warp tiles
 // amortise fragment loads and barriers
-double g_eff[NCFG] = {0.98, 1.00, 0.96, 0.90, 0.96, 0.90, 0.975};
+double g_eff[NCFG] = {0.98, 1.00, 0.96, 0.90, 0.96, 0.90, 0.975, 1.045, 0.99, 0.93};
+bool g_tma_enabled = true;
 int g_force_cfg = -1, g_force_split = 0;
 
 struct Entry {
   KFn fn = nullptr;
   int threads = 0, smem = 0, occ = 0;
   bool ready = false;
+  bool tma = false;
 };
 Entry g_table[NCFG][2][2][3];
 bool g_table_init = false;
@@ -117,6 +135,19 @@ void put_all(int ci) {
   put<C, 1, 1, 0>(ci); put<C, 1, 1, 2>(ci);
 }
 
+template <class T>
+void put_tma(int ci) {
+  const TmaFn fns[3] = {T::template fn<EPI_STORE>(), T::template fn<EPI_FILTER>(),
+                        T::template fn<EPI_PARTIAL>()};
+  for (int e = 0; e < 3; ++e) {
+    Entry& en = g_table[ci][OP_N][OP_N][e];
+    en.fn = reinterpret_cast<KFn>(fns[e]);
+    en.threads = T::threads;
+    en.smem = T::smem();
+    en.tma = true;
+  }
+}
+
 int ensure_table() {
   if (g_table_init) return OK;
   put_all<C0>(0);
@@ -126,6 +157,9 @@ int ensure_table() {
   put_all<C4>(4);
   put_all<C5>(5);
   put_all<C6>(6);
+  put_tma<T7>(7);
+  put_tma<T8>(8);
+  put_tma<T9>(9);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -157,6 +191,7 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   const int sms = h->sm_count;
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
+    if (c >= FIRST_TMA && !g_tma_enabled) continue;
     const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
     if (!e.ready && !ep.ready) continue;
@@ -192,6 +227,57 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   return best;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// Column-major complex matrix (rows x cols, ld) seen as a 2-D FP64 tensor
+// {2*rows doubles, cols}, box {16 doubles = 8 complex rows, box_cols}, 128-B swizzle.
+int encode_colmajor(CUtensorMap* map, const double2* base, long long rows, long long cols,
+                    long long ld, int box_rows, int box_cols) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled entry point unavailable");
+    return ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)(2 * rows), (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 16)};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * box_rows), (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return ERR_CUDA;
+  }
+  return OK;
+}
+
+int run_kernel(Handle* h, int c, const Entry& e, dim3 grid, const GemmParams& p) {
+  if (!e.tma) {
+    e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
+  } else {
+    // A: M x K (8-row boxes, BK = 8 columns); B: K x N (BK rows, BN columns)
+    CUtensorMap ma, mb;
+    CHFSI_TRY(encode_colmajor(&ma, p.A, p.M, p.K, p.lda, 8, kBKc[c]));
+    CHFSI_TRY(encode_colmajor(&mb, p.B, p.K, p.N, p.ldb, kBKc[c], kBN[c]));
+    reinterpret_cast<TmaFn>(e.fn)<<<grid, e.threads, e.smem, h->stream>>>(ma, mb, p);
+  }
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
 int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
            GemmParams p) {
   CHFSI_TRY(ensure_table());
@@ -213,12 +299,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.group = 1;
   const unsigned ntiles = (unsigned)((long long)p.tiles_m * p.tiles_n);
   if (pl.split == 1) {
-    const Entry& e = g_table[c][opa][opb][epi];
-    dim3 grid(ntiles, 1, 1);
-    e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
-    h->launches++;
-    CHFSI_CHECK_LAUNCH();
-    return OK;
+    return run_kernel(h, c, g_table[c][opa][opb][epi], dim3(ntiles, 1, 1), p);
   }
   const size_t ws_bytes = (size_t)pl.split * M * N * sizeof(double2);
   double2* ws = (double2*)scratch(h, SLOT_SPLITK, ws_bytes);
@@ -226,11 +307,8 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   GemmParams q = p;
   q.k_chunk = pl.k_chunk;
   q.ws = ws;
-  const Entry& e = g_table[c][opa][opb][EPI_PARTIAL];
-  dim3 grid(ntiles, 1, (unsigned)pl.split);
-  e.fn<<<grid, e.threads, e.smem, h->stream>>>(q);
-  h->launches++;
-  CHFSI_CHECK_LAUNCH();
+  CHFSI_TRY(run_kernel(h, c, g_table[c][opa][opb][EPI_PARTIAL], dim3(ntiles, 1, (unsigned)pl.split),
+                       q));
   const long long total = M * N;
   const int threads = 256;
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);

@@ -1,0 +1,236 @@
+// TMA + mbarrier pipelined complex128 DMMA GEMM for op(A) = op(B) = N (sm_100a).
+//
+// Same arithmetic and epilogues as zgemm.cuh (EPI_STORE / EPI_FILTER /
+// EPI_PARTIAL), different data movement:
+//   * operand tiles arrive by cp.async.bulk.tensor (TMA, SASS UTMALDG) into a
+//     STAGES-deep ring, 128-byte swizzled, completion tracked by an mbarrier
+//     transaction count (no LDGSTS address math in the consumer warps);
+//   * stage reuse is released by per-warp mbarrier arrivals, so there is no
+//     CTA-wide __syncthreads in the main loop; the refill of a stage is issued
+//     by lane 0 of warp (kt mod 4), spreading the producer duty;
+//   * 128B swizzle XORs the 16-byte chunk index with the 128-byte row index.
+//     Reading fragment row r from tile row p(r) = (r>>1) | ((r&1)<<2) makes
+//     every LDS.128 quarter-warp hit 8 distinct bank groups; the epilogue
+//     applies the same permutation to output rows and columns.
+//
+// Layouts (complex = 16 B; "row" = 128 B):
+//   A tile (column-major A, BM/8 boxes of {8 rows, BK cols}, box g at g*BK rows):
+//     chunk(mg, k, m8) = (mg*BK + k)*8 + (m8 ^ (k & 7))
+//   B tile (column-major B, box {BK rows, BN cols}):
+//     chunk(n, k)      = n*8 + (k ^ (n & 7))               (BK == 8)
+#pragma once
+
+#include <cuda.h>
+
+#include "zgemm.cuh"
+
+namespace chfsi {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); }
+
+template <int BM, int BN, int WM, int WN, int STAGES>
+constexpr int zgemm_tma_smem_bytes() {
+  return STAGES * (BM * 8 + BN * 8) * 16 + 1024 /* alignment slack */ + 2 * STAGES * 8;
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int EPI>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 const GemmParams p) {
+  constexpr int BK = 8;
+  constexpr int NWM = BM / WM;
+  constexpr int NWARP = NWM * (BN / WN);
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
+  constexpr unsigned STAGE_BYTES = (A_ELEMS + B_ELEMS) * 16;
+  static_assert((A_ELEMS * 16) % 1024 == 0 && (B_ELEMS * 16) % 1024 == 0, "1 KB aligned tiles");
+
+  extern __shared__ unsigned char smem_raw[];
+  double2* base = reinterpret_cast<double2*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double2* sA = base;
+  double2* sB = base + STAGES * A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_ELEMS);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % NWM, wn = warp / NWM;
+  int mi, ni;
+  tile_coords(p, blockIdx.x, mi, ni);
+  const int m0 = mi * BM, n0 = ni * BN;
+  int kbeg = 0, kend = p.K;
+  if (EPI == EPI_PARTIAL) {
+    kbeg = blockIdx.z * p.k_chunk;
+    kend = min(p.K, kbeg + p.k_chunk);
+  }
+  const int KT = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+
+  if (tid == 0) {
+    #pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  __syncthreads();
+
+  auto issue = [&](int kt) {
+    const int s = kt % STAGES;
+    const int k0 = kbeg + kt * BK;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    // A: one {8 rows x BK cols} box per 8-row group (coords in doubles, columns);
+    // B: one {BK rows x BN cols} box. Out-of-range rows/cols arrive zero-filled.
+    #pragma unroll
+    for (int g = 0; g < BM / 8; ++g)
+      tma_load_2d(sA + s * A_ELEMS + g * BK * 8, &mapA, 2 * (m0 + 8 * g), k0, &full[s]);
+    tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
+  };
+
+  if (tid == 0) {
+    #pragma unroll
+    for (int s = 0; s < STAGES; ++s)
+      if (s < KT) issue(s);
+  }
+
+  double cr[FM][FN][2], ci[FM][FN][2];
+  #pragma unroll
+  for (int i = 0; i < FM; ++i)
+    #pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      cr[i][j][0] = cr[i][j][1] = 0.0;
+      ci[i][j][0] = ci[i][j][1] = 0.0;
+    }
+
+  const int fr = lane >> 2, fc = lane & 3;
+  const int pr = perm8(fr);
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    const unsigned phase = (kt / STAGES) & 1;
+    mbar_wait(&full[s], phase);
+    const double2* a = sA + s * A_ELEMS;
+    const double2* b = sB + s * B_ELEMS;
+    #pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int kk = ks * 4 + fc;
+      double2 fa[FM], fb[FN];
+      #pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const int mg = (wm * WM) / 8 + i;
+        fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
+      }
+      #pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const int nn = wn * WN + j * 8 + pr;
+        fb[j] = b[nn * 8 + (kk ^ pr)];
+      }
+      #pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const double ar = fa[i].x, ai = fa[i].y, nai = -fa[i].y;
+        #pragma unroll
+        for (int j = 0; j < FN; ++j) {
+          dmma884(cr[i][j][0], cr[i][j][1], ar, fb[j].x);
+          dmma884(ci[i][j][0], ci[i][j][1], ar, fb[j].y);
+          dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
+          dmma884(ci[i][j][0], ci[i][j][1], ai, fb[j].x);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill this stage with tile kt + STAGES once every warp has released it
+    if (lane == 0 && warp == (kt % NWARP) && kt + STAGES < KT) {
+      mbar_wait(&empty[s], phase);
+      issue(kt + STAGES);
+    }
+  }
+
+  // epilogue: fragment row r <-> tile row perm8(r); fragment column c <-> perm8(c)
+  #pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int m = m0 + wm * WM + i * 8 + pr;
+    if (m >= p.M) continue;
+    #pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      #pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int n = n0 + wn * WN + j * 8 + perm8(fc * 2 + t);
+        if (n >= p.N) continue;
+        const double xr = cr[i][j][t], xi = ci[i][j][t];
+        if (EPI == EPI_PARTIAL) {
+          p.ws[(long long)blockIdx.z * p.M * p.N + m + (long long)n * p.M] = make_double2(xr, xi);
+        } else if (EPI == EPI_FILTER) {
+          const double2 y1 = p.B[m + (long long)n * p.ldb];
+          double orr = p.alpha.x * xr + p.beta.x * y1.x;
+          double oi = p.alpha.x * xi + p.beta.x * y1.y;
+          if (p.Y0 != nullptr) {
+            const double2 y0 = p.Y0[m + (long long)n * p.ld0];
+            orr += p.gamma * y0.x;
+            oi += p.gamma * y0.y;
+          }
+          p.C[m + (long long)n * p.ldc] = make_double2(orr, oi);
+        } else {
+          double2 o = make_double2(p.alpha.x * xr - p.alpha.y * xi, p.alpha.x * xi + p.alpha.y * xr);
+          if (p.beta.x != 0.0 || p.beta.y != 0.0) {
+            const double2 c = p.C[m + (long long)n * p.ldc];
+            o.x += p.beta.x * c.x - p.beta.y * c.y;
+            o.y += p.beta.x * c.y + p.beta.y * c.x;
+          }
+          p.C[m + (long long)n * p.ldc] = o;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace chfsi
