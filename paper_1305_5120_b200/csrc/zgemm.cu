@@ -91,16 +91,18 @@ using C5 = CfgT<128, 64, 8, 32, 32, 4>;
 using C6 = CfgT<128, 32, 8, 32, 16, 4>;
 // cfg 7: TMA 64x32 warp 32x16, 4 stages; cfg 8: TMA 64x16 warp 16x16; cfg 9: TMA 64x64 warp 32x32
 using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmParams);
-template <int BM, int BN, int WM, int WN, int ST>
+template <int BM, int BN, int WM, int WN, int ST, int MINB = 1>
 struct TmaT {
   static constexpr int threads = (BM / WM) * (BN / WN) * 32;
   static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST>(); }
   template <int EPI>
-  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI>; }
+  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB>; }
 };
-using T7 = TmaT<64, 32, 32, 16, 4>;
-using T8 = TmaT<64, 16, 16, 16, 4>;
-using T9 = TmaT<64, 64, 32, 32, 4>;
+// (explicit min-blocks keep ptxas at <= 128 regs -> 4 CTAs / SM for the 64x32 tile;
+// a register-double-buffered fragment variant measured 1.5-2 % slower, profiles/r01)
+using T7 = TmaT<64, 32, 32, 16, 4, 4>;
+using T8 = TmaT<64, 16, 16, 16, 4, 4>;
+using T9 = TmaT<64, 64, 32, 32, 4, 2>;
 const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64};
 const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64};
 const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8};

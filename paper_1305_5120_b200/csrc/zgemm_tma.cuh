@@ -81,8 +81,8 @@ constexpr int zgemm_tma_smem_bytes() {
   return STAGES * (BM * 8 + BN * 8) * 16 + 1024 /* alignment slack */ + 2 * STAGES * 8;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int EPI>
-__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32)
+template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1>
+__global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const GemmParams p) {
   constexpr int BK = 8;
@@ -174,15 +174,23 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         const int nn = wn * WN + j * 8 + pr;
         fb[j] = b[nn * 8 + (kk ^ pr)];
       }
+      // two sweeps over the warp tile: the second update of each accumulator is
+      // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
       #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        const double ar = fa[i].x, ai = fa[i].y, nai = -fa[i].y;
         #pragma unroll
         for (int j = 0; j < FN; ++j) {
-          dmma884(cr[i][j][0], cr[i][j][1], ar, fb[j].x);
-          dmma884(ci[i][j][0], ci[i][j][1], ar, fb[j].y);
+          dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
+          dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
+        }
+      }
+      #pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const double nai = -fa[i].y;
+        #pragma unroll
+        for (int j = 0; j < FN; ++j) {
           dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
-          dmma884(ci[i][j][0], ci[i][j][1], ai, fb[j].x);
+          dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
         }
       }
     }
