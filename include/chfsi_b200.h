@@ -86,10 +86,11 @@ int chfsi_orthonormalize(chfsi_handle_t h, int64_t n, int64_t k, void* d_F, int6
                          double* h_fro);
 
 /* core.py:318-330 `_rr_raw`: HQ = H Q, G = Q^H HQ, G <- (G+G^H)/2, (w, W) = eig(G)
- * (cuSOLVER zheevd, ascending), Z = Q W, HZ = HQ W. Ritz values to h_w (k). */
+ * (cuSOLVER zheevd, ascending), Z = Q W, HZ = HQ W. Ritz values to h_w (k); when h_res
+ * is not NULL also the residual norms ||HZ_j - w_j Z_j|| of core.py:477 (one host sync). */
 int chfsi_rayleigh_ritz(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
                         const void* d_Q, int64_t ldq, void* d_HQ, int64_t ldhq, void* d_Z,
-                        int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w);
+                        int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w, double* h_res);
 
 /* r_j = ||HY_j - lam_j Y_j||_2, core.py:347-358 `residuals` and core.py:477. */
 int chfsi_residual_norms(chfsi_handle_t h, int64_t n, int64_t k, const void* d_HY, int64_t ldhy,

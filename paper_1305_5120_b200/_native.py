@@ -49,7 +49,8 @@ SIGNATURES = {
     "chfsi_orthonormalize": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                      _i64, _c_void_p, _i64, _c_void_p, _i64, _dbl, _pi64, _pdbl]),
     "chfsi_rayleigh_ritz": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
-                                    _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64, _pdbl]),
+                                    _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64, _pdbl,
+                                    _pdbl]),
     "chfsi_residual_norms": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                      _pdbl, _pdbl]),
     "chfsi_hermitian_norms": (_int, [_c_void_p, _i64, _c_void_p, _i64, _pdbl]),

@@ -423,6 +423,7 @@ class DeviceSolver:
         locked_vals = []
         nl = 0
         act = ws.z[:s_tot]  # the unconverged block, a contiguous column range of Z
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         for it in range(1, cfg.max_outer_iters + 1):
             if not lam_ref < a_edge:
                 raise FilterDegenerate(
@@ -432,27 +433,27 @@ class DeviceSolver:
                 b_up = a_edge + max(1.0, abs(a_edge)) * 1e-8
             ncols = dev.cols(act)
 
-            t0 = time.perf_counter()
+            # phase times from CUDA events on the solver stream: the iteration needs
+            # only two host syncs (rank test after CholQR2; Ritz values + residuals)
+            ev[0].record(self.eng.stream)
             f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref)
-            self._sync()
-            tf = time.perf_counter() - t0
+            ev[1].record(self.eng.stream)
             _count_products(cfg.degree * ncols)
             report.filter_flops += 8.0 * n * n * cfg.degree * ncols
 
-            t0 = time.perf_counter()
             q = self._orthonormalize(f, ws.locked[:nl] if nl else None, ws.hq[:ncols],
                                      ws.fa[:ncols], rng)
-            self._sync()
-            tq = time.perf_counter() - t0
+            ev[2].record(self.eng.stream)
 
-            t0 = time.perf_counter()
-            w = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols], ws.hz[:ncols])
+            w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
+                                            ws.hz[:ncols], residuals=True)
+            ev[3].record(self.eng.stream)
             _count_products(ncols)
-            trr = time.perf_counter() - t0
-
-            t0 = time.perf_counter()
-            res = self.eng.residual_norms(ws.hz[:ncols], ws.z[:ncols], w)
-            tres = time.perf_counter() - t0
+            ev[3].synchronize()
+            tf = ev[0].elapsed_time(ev[1]) * 1e-3
+            tq = ev[1].elapsed_time(ev[2]) * 1e-3
+            trr = ev[2].elapsed_time(ev[3]) * 1e-3  # includes the fused residual norms
+            tres = 0.0
 
             kk = 0
             while kk < len(w) and res[kk] < cfg.tol and len(locked_vals) < nev:

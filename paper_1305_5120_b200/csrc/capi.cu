@@ -67,7 +67,7 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
                    double* fro_out);
 int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long long ldh,
                   const double2* Q, long long ldq, double2* HQ, long long ldhq, double2* Z,
-                  long long ldz, double2* HZ, long long ldhz, double* w_dev);
+                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host);
 
 // ---------------------------------------------------------------- peaks
 // Register-resident 4 x 4 block of independent 8x8 accumulators fed by 4 A and
@@ -279,15 +279,11 @@ int chfsi_orthonormalize(chfsi_handle_t h, int64_t n, int64_t k, void* d_F, int6
 
 int chfsi_rayleigh_ritz(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
                         const void* d_Q, int64_t ldq, void* d_HQ, int64_t ldhq, void* d_Z,
-                        int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w) {
+                        int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w, double* h_res) {
   H_CHECK(h);
-  double* w = (double*)scratch(h, SLOT_VEC, (size_t)(k + 8) * sizeof(double));
-  if (!w) return ERR_NOMEM;
-  CHFSI_TRY(rayleigh_ritz(h, n, k, (const double2*)d_H, ldh, (const double2*)d_Q, ldq,
-                          (double2*)d_HQ, ldhq, (double2*)d_Z, ldz, (double2*)d_HZ, ldhz, w));
-  CHFSI_CUDA(cudaMemcpyAsync(h_w, w, k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
-  return OK;
+  if (k <= 0) return OK;
+  return rayleigh_ritz(h, n, k, (const double2*)d_H, ldh, (const double2*)d_Q, ldq,
+                       (double2*)d_HQ, ldhq, (double2*)d_Z, ldz, (double2*)d_HZ, ldhz, h_w, h_res);
 }
 
 int chfsi_residual_norms(chfsi_handle_t h, int64_t n, int64_t k, const void* d_HY, int64_t ldhy,

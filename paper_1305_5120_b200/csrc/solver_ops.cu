@@ -187,31 +187,50 @@ int lanczos_bound(Handle* h, long long n, int k, const double2* H, long long ldh
   return OK;
 }
 
-// One Cholesky-QR pass: out = X R^-1 where X^H X = R^H R (+ shift I).
-// diag_host receives the real diagonal of R. Returns ERR_NOT_PD (detail=pivot) on failure.
-static int cholqr_pass(Handle* h, long long n, long long k, const double2* X, long long ldx,
-                       double2* out, long long ldo, double shift, double* diag_host,
-                       int* pivot) {
+// One Cholesky-QR pass, fully stream-ordered (no host sync):
+//   G = X^H X (+ shift I); G = L L^H (zpotrf, info -> info_dev); diag(L) -> diag_dev;
+//   out = X L^-H  (R = L^H, so R^-1 = (L^-1)^H).
+// A failed factorisation leaves garbage in `out`; callers check info after one sync.
+static int cholqr_pass_async(Handle* h, long long n, long long k, const double2* X, long long ldx,
+                             double2* out, long long ldo, double shift, double* diag_dev,
+                             int* info_dev) {
   double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
   double2* Li = (double2*)scratch(h, SLOT_SMALL2, (size_t)k * k * sizeof(double2));
-  double* dv = (double*)scratch(h, SLOT_VEC, (size_t)(k + 8) * sizeof(double));
-  if (!G || !Li || !dv) return ERR_NOMEM;
+  if (!G || !Li) return ERR_NOMEM;
   CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, X, ldx, X, ldx, ZERO, G, k));
   CHFSI_TRY(hermitize(h, k, G, k));
   if (shift != 0.0) CHFSI_TRY(shift_diag(h, k, G, k, shift));
-  int info = 0;
-  CHFSI_TRY(potrf_lower(h, k, G, k, &info));
-  if (info != 0) {
-    *pivot = info;
-    return ERR_NOT_PD;
-  }
-  CHFSI_TRY(get_real_diag(h, k, G, k, dv));
-  CHFSI_CUDA(cudaMemcpyAsync(diag_host, dv, k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  int lwork = 0;
+  CHFSI_SOLVER(cusolverDnZpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, (int)k,
+                                           (cuDoubleComplex*)G, (int)k, &lwork));
+  void* work = scratch(h, SLOT_SOLVER, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+  if (!work) return ERR_NOMEM;
+  CHFSI_SOLVER(cusolverDnZpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, (int)k, (cuDoubleComplex*)G,
+                                (int)k, (cuDoubleComplex*)work, lwork, info_dev));
+  h->launches++;
+  CHFSI_TRY(get_real_diag(h, k, G, k, diag_dev));
   CHFSI_TRY(trtri_lower(h, k, G, k, Li, k));
-  // R^-1 = (L^H)^-1 = (L^-1)^H
   CHFSI_TRY(zgemm(h, OP_N, OP_C, n, k, k, ONE, X, ldx, Li, k, ZERO, out, ldo));
-  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
   return OK;
+}
+
+// Device-side small-vector block of one orthonormalisation, copied to the host in one go.
+struct OrthVec {
+  double* dots;  // 2k doubles (complex column self-dots)
+  double* d[3];  // k each: diag(R) of up to three passes
+  int* info;     // 3 ints
+  size_t bytes;
+};
+
+static OrthVec orth_vec_layout(double* base, long long k) {
+  OrthVec v;
+  v.dots = base;
+  v.d[0] = base + 2 * k;
+  v.d[1] = base + 3 * k;
+  v.d[2] = base + 4 * k;
+  v.info = reinterpret_cast<int*>(base + 5 * k);
+  v.bytes = (size_t)(5 * k) * sizeof(double) + 4 * sizeof(int);
+  return v;
 }
 
 int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ldf,
@@ -228,56 +247,48 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
       CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, nl, MONE, Lk, ldl, P, nl, ONE, F, ldf));
     }
   }
-  std::vector<double> d1(k), d2(k), d3(k);
-  // ||W||_F via column dots (deterministic), summed on the host in fixed order
-  {
-    double2* dots = (double2*)scratch(h, SLOT_SMALL2, (size_t)k * sizeof(double2));
-    if (!dots) return ERR_NOMEM;
-    CHFSI_TRY(zdotc_cols(h, n, k, F, ldf, F, ldf, dots));
-    std::vector<double2> hd(k);
-    CHFSI_CUDA(cudaMemcpyAsync(hd.data(), dots, k * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
-    CHFSI_CUDA(cudaStreamSynchronize(h->stream));
-    double s = 0.0;
-    for (long long j = 0; j < k; ++j) s += hd[j].x;
-    *fro_out = std::sqrt(s);
-  }
-  const double fro = *fro_out;
-  int pivot = 0;
-  int st = cholqr_pass(h, n, k, F, ldf, T, ldt, 0.0, d1.data(), &pivot);
+  double* vbase = (double*)scratch(h, SLOT_VEC, (size_t)(5 * k + 4) * sizeof(double));
+  if (!vbase) return ERR_NOMEM;
+  const OrthVec dv = orth_vec_layout(vbase, k);
+  double* hbase = pinned(h, dv.bytes);
+  if (!hbase) return ERR_NOMEM;
+  const OrthVec hv = orth_vec_layout(hbase, k);
+  CHFSI_CUDA(cudaMemsetAsync(dv.info, 0, 3 * sizeof(int), h->stream));
+  // ||W||_F via deterministic column dots; CholQR2 passes F -> T -> Q, all async
+  CHFSI_TRY(zdotc_cols(h, n, k, F, ldf, F, ldf, (double2*)dv.dots));
+  CHFSI_TRY(cholqr_pass_async(h, n, k, F, ldf, T, ldt, 0.0, dv.d[0], dv.info + 0));
+  CHFSI_TRY(cholqr_pass_async(h, n, k, T, ldt, Q, ldq, 0.0, dv.d[1], dv.info + 1));
+  CHFSI_CUDA(cudaMemcpyAsync(hbase, vbase, dv.bytes, cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));  // the one host sync of the fast path
+  double s = 0.0;
+  for (long long j = 0; j < k; ++j) s += hv.dots[2 * j];
+  const double fro = std::sqrt(s);
+  *fro_out = fro;
   bool shifted = false;
-  if (st == ERR_NOT_PD) {
-    // shifted CholQR (Fukaya et al.): s = 11 (n k + k (k+1)) u ||F||^2
+  if (hv.info[0] != 0) {
+    // first Cholesky broke down (ill-conditioned block): shifted CholQR3
+    // (Fukaya et al.), s = 11 (n k + k (k+1)) u ||F||^2, then two plain passes
     const double u = 1.1102230246251565e-16;
-    const double s = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro * fro;
-    st = cholqr_pass(h, n, k, F, ldf, T, ldt, s, d1.data(), &pivot);
+    const double sh = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro * fro;
+    CHFSI_CUDA(cudaMemsetAsync(dv.info, 0, 3 * sizeof(int), h->stream));
+    CHFSI_TRY(cholqr_pass_async(h, n, k, F, ldf, T, ldt, sh, dv.d[0], dv.info + 0));
+    CHFSI_TRY(cholqr_pass_async(h, n, k, T, ldt, Q, ldq, 0.0, dv.d[1], dv.info + 1));
+    CHFSI_TRY(cholqr_pass_async(h, n, k, Q, ldq, T, ldt, 0.0, dv.d[2], dv.info + 2));
+    CHFSI_TRY(zcopy2d(h, n, k, T, ldt, Q, ldq));
+    CHFSI_CUDA(cudaMemcpyAsync(hbase, vbase, dv.bytes, cudaMemcpyDeviceToHost, h->stream));
+    CHFSI_CUDA(cudaStreamSynchronize(h->stream));
     shifted = true;
   }
-  if (st == ERR_NOT_PD) {
-    *bad_col = pivot - 1;
-    set_error("rank collapse in column " + std::to_string(pivot - 1));
-    return ERR_RANK;
-  }
-  CHFSI_TRY(st);
-  st = cholqr_pass(h, n, k, T, ldt, Q, ldq, 0.0, d2.data(), &pivot);
-  if (st == ERR_NOT_PD) {
-    *bad_col = pivot - 1;
-    set_error("rank collapse in column " + std::to_string(pivot - 1));
-    return ERR_RANK;
-  }
-  CHFSI_TRY(st);
-  if (shifted) {
-    st = cholqr_pass(h, n, k, Q, ldq, T, ldt, 0.0, d3.data(), &pivot);
-    if (st == ERR_NOT_PD) {
-      *bad_col = pivot - 1;
-      set_error("rank collapse in column " + std::to_string(pivot - 1));
+  for (int pass = 0; pass < (shifted ? 3 : 2); ++pass) {
+    if (hv.info[pass] != 0) {
+      *bad_col = hv.info[pass] - 1;
+      set_error("rank collapse in column " + std::to_string(*bad_col));
       return ERR_RANK;
     }
-    CHFSI_TRY(st);
-    CHFSI_TRY(zcopy2d(h, n, k, T, ldt, Q, ldq));
   }
   for (long long j = 0; j < k; ++j) {
-    double r = std::fabs(d1[j] * d2[j]);
-    if (shifted) r *= std::fabs(d3[j]);
+    double r = std::fabs(hv.d[0][j] * hv.d[1][j]);
+    if (shifted) r *= std::fabs(hv.d[2][j]);
     if (r < rank_rel_tol * fro) {
       *bad_col = j;
       set_error("rank collapse in column " + std::to_string(j));
@@ -287,17 +298,45 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
   return OK;
 }
 
+// core.py:318-330 `_rr_raw` plus the residual norms of core.py:477, with a single
+// host sync: Ritz values, residuals and the zheevd info come back together.
 int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long long ldh,
                   const double2* Q, long long ldq, double2* HQ, long long ldhq, double2* Z,
-                  long long ldz, double2* HZ, long long ldhz, double* w_dev) {
+                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host) {
   double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
-  if (!G) return ERR_NOMEM;
+  double* v = (double*)scratch(h, SLOT_VEC, (size_t)(2 * k + 2) * sizeof(double));
+  if (!G || !v) return ERR_NOMEM;
+  double* w_dev = v;
+  double* r_dev = v + k;
+  int* info_dev = reinterpret_cast<int*>(v + 2 * k);
   CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, Q, ldq, ZERO, HQ, ldhq));
   CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, Q, ldq, HQ, ldhq, ZERO, G, k));
   CHFSI_TRY(hermitize(h, k, G, k));
-  CHFSI_TRY(heevd(h, k, G, k, w_dev));
+  int lwork = 0;
+  CHFSI_SOLVER(cusolverDnZheevd_bufferSize(h->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                           CUBLAS_FILL_MODE_LOWER, (int)k, (cuDoubleComplex*)G,
+                                           (int)k, w_dev, &lwork));
+  void* work = scratch(h, SLOT_SOLVER, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+  if (!work) return ERR_NOMEM;
+  CHFSI_SOLVER(cusolverDnZheevd(h->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                (int)k, (cuDoubleComplex*)G, (int)k, w_dev,
+                                (cuDoubleComplex*)work, lwork, info_dev));
+  h->launches++;
   CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, k, ONE, Q, ldq, G, k, ZERO, Z, ldz));
   CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, k, ONE, HQ, ldhq, G, k, ZERO, HZ, ldhz));
+  if (res_host) CHFSI_TRY(residual_norms(h, n, k, HZ, ldhz, Z, ldz, w_dev, r_dev));
+  const size_t bytes = (size_t)(2 * k) * sizeof(double) + sizeof(int);
+  double* hb = pinned(h, bytes + 16);
+  if (!hb) return ERR_NOMEM;
+  CHFSI_CUDA(cudaMemcpyAsync(hb, v, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  const int info = *reinterpret_cast<int*>(hb + 2 * k);
+  if (info != 0) {
+    set_error("zheevd failed to converge, info=" + std::to_string(info));
+    return ERR_CUSOLVER;
+  }
+  std::copy(hb, hb + k, w_host);
+  if (res_host) std::copy(hb + k, hb + 2 * k, res_host);
   return OK;
 }
 

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <unordered_map>
 
 #include "internal.h"
 #include "zgemm.cuh"
@@ -229,6 +230,38 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   return best;
 }
 
+// Plans are pure functions of (ops, epilogue, shape, overrides): memoise them so the
+// per-call host cost of a small GEMM is a hash lookup (the solve's tail issues
+// thousands of identical small products).
+struct PlanKey {
+  int opa, opb, epi, fcfg, fsplit;
+  long long M, N, K;
+  bool operator==(const PlanKey& o) const {
+    return opa == o.opa && opb == o.opb && epi == o.epi && fcfg == o.fcfg && fsplit == o.fsplit &&
+           M == o.M && N == o.N && K == o.K;
+  }
+};
+struct PlanKeyHash {
+  size_t operator()(const PlanKey& k) const {
+    size_t h = (size_t)k.M * 0x9E3779B97F4A7C15ULL;
+    h ^= (size_t)k.N * 0xC2B2AE3D27D4EB4FULL + (h << 6) + (h >> 2);
+    h ^= (size_t)k.K * 0x165667B19E3779F9ULL + (h << 6) + (h >> 2);
+    h ^= (size_t)(k.opa | (k.opb << 1) | (k.epi << 2) | ((k.fcfg + 1) << 4) | (k.fsplit << 9));
+    return h;
+  }
+};
+
+Plan cached_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
+  static std::unordered_map<PlanKey, Plan, PlanKeyHash> cache;
+  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, M, N, K};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  if (cache.size() > 65536) cache.clear();
+  cache.emplace(key, pl);
+  return pl;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -291,7 +324,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
-  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  const Plan pl = cached_plan(h, opa, opb, epi, M, N, K);
   const int c = pl.cfg;
   p.tiles_m = (int)((M + kBM[c] - 1) / kBM[c]);
   p.tiles_n = (int)((N + kBN[c] - 1) / kBN[c]);

@@ -159,13 +159,16 @@ class Engine:
         _native.check("chfsi_orthonormalize", st)
         return Q, float(fro.value)
 
-    def rayleigh_ritz(self, H, Q, HQ, Z, HZ):
+    def rayleigh_ritz(self, H, Q, HQ, Z, HZ, residuals=False):
+        """Ritz values (and, with residuals=True, ||HZ_j - w_j Z_j||) in one host sync."""
         n, k = rows(Q), cols(Q)
         w = np.empty(k, dtype=np.float64)
+        res = np.empty(k, dtype=np.float64) if residuals else None
+        pd = ctypes.POINTER(ctypes.c_double)
         _native.call("chfsi_rayleigh_ritz", self.h, n, k, ptr(H), ld(H), ptr(Q), ld(Q),
-                     ptr(HQ), ld(HQ), ptr(Z), ld(Z), ptr(HZ), ld(HZ),
-                     w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
-        return w
+                     ptr(HQ), ld(HQ), ptr(Z), ld(Z), ptr(HZ), ld(HZ), w.ctypes.data_as(pd),
+                     res.ctypes.data_as(pd) if residuals else None)
+        return (w, res) if residuals else w
 
     def residual_norms(self, HY, Y, lam):
         n, k = rows(Y), cols(Y)
