@@ -38,17 +38,27 @@ METRIC = "filter FP64 TFLOP/s (ChFSI Chebyshev filter, n=20000, k=nev+nex=2200, 
 UNIT = "TFLOP/s"
 
 
+def metric_name(args):
+    if (args.n, args.k, args.degree) == (20000, 2200, 25):
+        return METRIC
+    return (f"filter FP64 TFLOP/s (ChFSI Chebyshev filter, n={args.n}, k={args.k}, "
+            f"m={args.degree}; non-default test shape)")
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=20000)
-    ap.add_argument("--k", type=int, default=2200)
+    # (long names: torchrun's argparse would take "--n"/"--k" as abbreviations of its own)
+    ap.add_argument("--matrix-order", dest="n", type=int, default=20000)
+    ap.add_argument("--block-cols", dest="k", type=int, default=2200)
     ap.add_argument("--degree", type=int, default=25)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/tail/solve legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (gloo: host-staged, for testing)")
     return ap.parse_args()
 
 
@@ -170,7 +180,8 @@ def run_reference(args, rank, world):
     val = step_flops * args.steps / dt / 1e12
     cores = os.cpu_count()
     line = {
-        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": metric_name(args), "value": val, "unit": UNIT,
+        "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
         "data": "synthetic (seeded complex Gaussian Hermitian; c4 shape)",
@@ -278,9 +289,10 @@ def run_b200(args, rank, world, local_rank):
         return
     peaks = measured_fp64_peaks(local_rank)
     peak = peaks["dmma_tflops"]
-    traffic = committed_traffic()
+    traffic = committed_traffic(n, kp)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args), "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64 DMMA)",
         "data": "synthetic (seeded; H = Q diag(lambda) Q^H with the c0 spectrum recipe at n=20000)",
@@ -301,6 +313,7 @@ def run_b200(args, rank, world, local_rank):
         del H, Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         line["solve_c0"] = solve_c0()
+        line["sequence_c1"] = sequence_c1()
         line["c4_outer_iteration"] = c4_iteration_window()
         torch.cuda.empty_cache()
         rate, sample, cores = cpu_filter_rate(n, m, args.cpu_seconds)
@@ -367,12 +380,15 @@ def measured_fp64_peaks(index):
     return {"dmma_tflops": dm, "dfma_tflops": df, "nominal_fp64_tflops_at_max_clock": nominal}
 
 
-def committed_traffic():
-    """dram bytes per launch from the committed ncu --set full capture, if present."""
+def committed_traffic(n, k):
+    """DRAM bytes per launch from the committed ncu --set full capture of the same
+    launch shape (profiles/filter_kernel_ncu.json), else None."""
     p = os.path.join(ROOT, "profiles", "filter_kernel_ncu.json")
     try:
         with open(p) as f:
             d = json.load(f)
+        if (d.get("n"), d.get("k")) != (n, k):
+            return None
         return d.get("dram_bytes_per_launch")
     except Exception:
         return None
@@ -432,19 +448,43 @@ def tail_widths(eng, H, n, dev):
 
 
 def solve_c0():
-    """s per ChFSI solve at BASELINE config 0 (n=1000, nev=100, nex=20, m=15, random start),
-    reference interval semantics; the reference CPU needed 2524 iterations / ~60 s."""
+    """s per ChFSI solve at BASELINE config 0 (n=1000, nev=100, nex=20, m=15, random start;
+    generator seed 0, solver seed 1). The reference CPU needed 2524 iterations / 60.6 s
+    here (tests/golden/c0.npz). Reported for the reference interval placement and for the
+    opt-in block_top placement (SURVEY.md section 7 ii)."""
     import paper_1305_5120_b200 as G
     from paper_1305_5120_b200.workloads import baseline_matrix
     h, lam_true, _ = baseline_matrix(0, 1000)
-    cfg = G.SolverConfig(nev=100, buffer=20, degree=15, max_outer_iters=20000)
-    t0 = time.perf_counter()
-    lam, vecs, rep = G.chfsi_solve(h, None, cfg, seed=1)
-    dt = time.perf_counter() - t0
-    return {"s_per_solve": dt, "outer_iterations": rep.outer_iterations,
+    out = {"reference_cpu_s": 60.6, "reference_cpu_iterations": 2524}
+    for interval in ("reference", "block_top"):
+        cfg = G.SolverConfig(nev=100, buffer=20, degree=15, max_outer_iters=20000,
+                             interval=interval)
+        t0 = time.perf_counter()
+        lam, vecs, rep = G.chfsi_solve(h, None, cfg, seed=1)
+        dt = time.perf_counter() - t0
+        out[interval] = {
+            "s_per_solve": dt, "outer_iterations": rep.outer_iterations,
+            "total_matmuls": rep.total_matmuls,
             "max_rel_eig_err_vs_exact": float(np.max(np.abs(lam - lam_true[:100]) / np.abs(lam_true[:100]))),
-            "filter_tflops": rep.filter_tflops, "t_filter": rep.t_filter, "t_qr": rep.t_qr,
-            "t_rr": rep.t_rr, "t_resid": rep.t_resid}
+            "t_filter": rep.t_filter, "t_qr": rep.t_qr, "t_rr": rep.t_rr}
+    return out
+
+
+def sequence_c1():
+    """BASELINE config 1: 5 correlated n=2000 problems (delta = 1e-3 ||H_1||), nev=200, nex=40,
+    m=20, eigenvector reuse through solve_sequence; s per sequence (reference CPU: ~999 s)."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    probs = baseline_sequence(0, 2000, 5)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=2000, N=5, nev=200, seed=0),
+                            problems=[(a, None) for a, _ in probs])
+    cfg = G.SolverConfig(nev=200, buffer=40, degree=20, max_outer_iters=20000)
+    t0 = time.perf_counter()
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
+    dt = time.perf_counter() - t0
+    return {"s_per_sequence": dt, "reference_cpu_s": 999.0,
+            "iterations": [r.outer_iterations for r in rep.reports],
+            "work": rep.work, "filter_s": sum(r.t_filter for r in rep.reports)}
 
 
 def main():
@@ -458,8 +498,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        if args.dist_backend == "gloo":
+            # test mode: ranks may share a GPU (host-staged gather, no waiting kernels)
+            local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     run_b200(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
