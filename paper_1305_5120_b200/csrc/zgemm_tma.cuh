@@ -154,52 +154,115 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 
   const int fr = lane >> 2, fc = lane & 3;
   const int pr = perm8(fr);
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % STAGES;
-    const unsigned phase = (kt / STAGES) & 1;
-    mbar_wait(&full[s], phase);
-    const double2* a = sA + s * A_ELEMS;
-    const double2* b = sB + s * B_ELEMS;
-    #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int kk = ks * 4 + fc;
-      double2 fa[FM], fb[FN];
+  // 8-column MMA blocks of this warp that hold at least one real column: blocks
+  // entirely past N (the padded tail of a narrow filter block) issue no DMMAs.
+  // Warp-uniform, so DMMA's warp-collective semantics are kept.
+  const int jvalid = min(FN, max(0, (p.N - (n0 + wn * WN) + 7) / 8));
+  if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      const unsigned phase = (kt / STAGES) & 1;
+      mbar_wait(&full[s], phase);
+      const double2* a = sA + s * A_ELEMS;
+      const double2* b = sB + s * B_ELEMS;
       #pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        const int mg = (wm * WM) / 8 + i;
-        fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
-      }
-      #pragma unroll
-      for (int j = 0; j < FN; ++j) {
-        const int nn = wn * WN + j * 8 + pr;
-        fb[j] = b[nn * 8 + (kk ^ pr)];
-      }
-      // two sweeps over the warp tile: the second update of each accumulator is
-      // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
-      #pragma unroll
-      for (int i = 0; i < FM; ++i) {
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int kk = ks * 4 + fc;
+        double2 fa[FM], fb[FN];
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int mg = (wm * WM) / 8 + i;
+          fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
+        }
         #pragma unroll
         for (int j = 0; j < FN; ++j) {
-          dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
-          dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
+          const int nn = wn * WN + j * 8 + pr;
+          fb[j] = b[nn * 8 + (kk ^ pr)];
+        }
+        // two sweeps over the warp tile: the second update of each accumulator is
+        // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            {
+              dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
+              dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
+            }
+          }
+        }
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const double nai = -fa[i].y;
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            {
+              dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
+              dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
+            }
+          }
         }
       }
-      #pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        const double nai = -fa[i].y;
-        #pragma unroll
-        for (int j = 0; j < FN; ++j) {
-          dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
-          dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
-        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill this stage with tile kt + STAGES once every warp has released it
+      if (lane == 0 && warp == (kt % NWARP) && kt + STAGES < KT) {
+        mbar_wait(&empty[s], phase);
+        issue(kt + STAGES);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    // refill this stage with tile kt + STAGES once every warp has released it
-    if (lane == 0 && warp == (kt % NWARP) && kt + STAGES < KT) {
-      mbar_wait(&empty[s], phase);
-      issue(kt + STAGES);
+  } else {  // ragged column edge: skip 8-column blocks past N
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = kt % STAGES;
+      const unsigned phase = (kt / STAGES) & 1;
+      mbar_wait(&full[s], phase);
+      const double2* a = sA + s * A_ELEMS;
+      const double2* b = sB + s * B_ELEMS;
+      #pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int kk = ks * 4 + fc;
+        double2 fa[FM], fb[FN];
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int mg = (wm * WM) / 8 + i;
+          fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
+        }
+        #pragma unroll
+        for (int j = 0; j < FN; ++j) {
+          const int nn = wn * WN + j * 8 + pr;
+          fb[j] = b[nn * 8 + (kk ^ pr)];
+        }
+        // two sweeps over the warp tile: the second update of each accumulator is
+        // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            if (j < jvalid) {
+              dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
+              dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
+            }
+          }
+        }
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const double nai = -fa[i].y;
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            if (j < jvalid) {
+              dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
+              dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      // refill this stage with tile kt + STAGES once every warp has released it
+      if (lane == 0 && warp == (kt % NWARP) && kt + STAGES < KT) {
+        mbar_wait(&empty[s], phase);
+        issue(kt + STAGES);
+      }
     }
   }
 
