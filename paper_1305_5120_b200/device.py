@@ -34,7 +34,14 @@ def ld(t):
 
 
 def ptr(t):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+    """Raw device pointer for the C ABI. torch's lazy conjugate/negative views share
+    storage with their source (the bit is not applied to memory), so they must be
+    materialised (``resolve_conj()``) before the kernels may read them."""
+    if t is None:
+        return ctypes.c_void_p(0)
+    if t.is_conj() or t.is_neg():
+        raise ValueError("tensor has a lazy conj/neg bit; call resolve_conj()/resolve_neg() first")
+    return ctypes.c_void_p(t.data_ptr())
 
 
 def empty(n, k, device):

@@ -140,7 +140,8 @@ def spectrum_matrix_torch(seed, n, device):
     del q
     h = (h + h.conj().T) / 2
     # h is Hermitian: its row-major storage is conj(H) column-major; store H^T = conj(H)
-    # rows so that row j of the tensor is column j of H.
-    hc = h.conj().contiguous()
+    # rows so that row j of the tensor is column j of H. (conj() is a lazy view in
+    # torch: resolve_conj() writes the conjugated values to memory.)
+    hc = h.conj().resolve_conj().contiguous()
     del h
     return hc, lam

@@ -218,3 +218,83 @@ def test_cholesky_trtri_heevd(eng):
     d = D.to_device(h, eng.device)
     w = eng.heevd(d)
     assert np.max(np.abs(w - np.linalg.eigvalsh(h))) <= 1e-13 * np.max(np.abs(w))
+
+
+# every tile configuration and split factor the cost model can pick, on ragged shapes
+_NCFG = 10
+_TMA_FIRST = 7
+
+
+@pytest.mark.parametrize("cfg", list(range(_NCFG)))
+@pytest.mark.parametrize("split", [1, 3])
+def test_every_gemm_config_and_split(eng, cfg, split):
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    rng = np.random.default_rng(100 + cfg * 7 + split)
+    ops = [("N", "N")] if cfg >= _TMA_FIRST else [("N", "N"), ("C", "N"), ("N", "C"), ("C", "C")]
+    try:
+        assert lib.chfsi_gemm_override(cfg, split) == 0
+        for (m, n, k) in [(70, 37, 203), (8, 8, 8), (129, 1, 300), (5, 66, 1029)]:
+            for opa, opb in ops:
+                A = crand(rng, m, k) if opa == "N" else crand(rng, k, m)
+                B = crand(rng, k, n) if opb == "N" else crand(rng, n, k)
+                C = crand(rng, m, n)
+                ref = (0.3 + 0.1j) * ((A if opa == "N" else A.conj().T) @
+                                      (B if opb == "N" else B.conj().T)) + (0.5 - 0.2j) * C
+                dC = D.to_device(C, eng.device)
+                eng.zgemm(opa, opb, m, n, k, 0.3 + 0.1j, D.to_device(A, eng.device),
+                          D.to_device(B, eng.device), 0.5 - 0.2j, dC)
+                got = D.to_host(dC)
+                assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref), (m, n, k, opa, opb)
+            # fused filter epilogue (square A, in place over Y0)
+            if m == k or cfg >= 0:
+                H = crand(rng, m, m)
+                Y1, Y0 = crand(rng, m, n), crand(rng, m, n)
+                dY0 = D.to_device(Y0, eng.device)
+                eng.filter_step(D.to_device(H, eng.device), D.to_device(Y1, eng.device),
+                                0.7, -0.2, dY0, 0.1, dY0)
+                ref = 0.7 * (H @ Y1) - 0.2 * Y1 + 0.1 * Y0
+                assert np.linalg.norm(D.to_host(dY0) - ref) <= 1e-13 * np.linalg.norm(ref)
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
+def test_plan_is_tma_for_the_filter_shape(eng):
+    import ctypes
+    from paper_1305_5120_b200 import _native
+    cfg, split = ctypes.c_int(), ctypes.c_int()
+    _native.call("chfsi_gemm_plan", eng.h, 0, 0, 1, 20000, 2200, 20000, ctypes.byref(cfg),
+                 ctypes.byref(split))
+    assert cfg.value >= _TMA_FIRST and split.value == 1
+
+
+def test_full_size_filter_on_exact_eigenvectors(eng):
+    """Size-independent property at BASELINE c4 size (n = 20000): for an exact
+    eigenvector q_j of H, p_m(H) q_j = p_m(lambda_j) q_j with the scalar closed form."""
+    import torch
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    n, m = 20000, 25
+    dev = eng.device
+    rng = np.random.default_rng(7)
+    lam = np.sort(np.concatenate([rng.uniform(-1.0, 0.0, n // 5),
+                                  10.0 ** rng.uniform(0.0, 2.0, n - n // 5)]))
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    q, _ = torch.linalg.qr(torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g))
+    lt = torch.as_tensor(lam, dtype=torch.complex128, device=dev)
+    h = (q * lt) @ q.conj().T
+    hb = ((h + h.conj().T) / 2).conj().resolve_conj().contiguous()  # column-major block of H
+    del h
+    cols = [0, 1, 1999, 2000, 2199, n - 1]
+    y = q[:, cols].T.contiguous()  # (k, n) block of exact eigenvectors
+    w = torch.empty_like(y)
+    a, b, lr = float(lam[2000]), float(lam[-1]) * 1.01, float(lam[0])
+    out = eng.filter(hb, y.clone(), w, m, a, b, lr)
+    got = out.cpu().numpy()
+    qs = q[:, cols].T.cpu().numpy()
+    gain = O.filter_gain(m, lam[cols], a, b, lr)
+    errs = [float(np.linalg.norm(got[r] - gain[r] * qs[r])) for r in range(len(cols))]
+    # FP64 budget: H = Q diag(lam) Q^H is exact only to ~1e-13 ||H|| at n = 20000, and
+    # the normalised recurrence (|p| <= 1 on the spectrum) carries that forward
+    assert max(errs) <= 1e-9, (errs, list(gain))

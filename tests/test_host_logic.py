@@ -118,6 +118,29 @@ def test_vector_angles_and_subspace_angle():
     assert abs(G.subspace_angle(e[:, :2], v) - eps) <= 1e-3 * eps
 
 
+def test_device_ptr_rejects_lazy_conj_views():
+    """torch's conj() is a lazy bit over shared storage: the C ABI must never see it."""
+    import torch
+    from paper_1305_5120_b200 import device as D
+    t = torch.randn((3, 4), dtype=torch.complex128)
+    with pytest.raises(ValueError):
+        D.ptr(t.conj())
+    assert D.ptr(t.conj().resolve_conj()).value is not None
+    assert D.ptr(None).value is None
+
+
+def test_block_layout_roundtrip():
+    """numpy F-order (n, k) <-> (k, n) column-major block, no transposition of values."""
+    import torch
+    from paper_1305_5120_b200 import device as D
+    a = np.arange(12, dtype=np.complex128).reshape(4, 3) * (1 + 2j)
+    t = D.to_device(a, torch.device("cpu"))
+    assert tuple(t.shape) == (3, 4) and D.rows(t) == 4 and D.cols(t) == 3 and D.ld(t) == 4
+    assert np.array_equal(t[1].numpy(), a[:, 1])
+    back = D.to_host(t)
+    assert back.flags.f_contiguous and np.array_equal(back, a)
+
+
 def test_attach_work_ratios():
     a = G.SequenceReport(mode="random", work=[10, 20, 30])
     b = G.SequenceReport(mode="reuse", work=[10, 10, 10])
