@@ -7,6 +7,7 @@
 // most SMs idle. Split-K partials are reduced in fixed z order, so results
 // are bit-identical run to run (reference criterion 7, test_acceptance.py:199).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -330,8 +331,23 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.tiles_n = (int)((N + kBN[c] - 1) / kBN[c]);
   // Row-major raster (consecutive CTAs share one H row strip). A grouped raster
   // (several row tiles per wave sharing Y strips) measured 1.5 % slower on B200
-  // (profiles/r01), so group = 1.
-  p.group = 1;
+  // with the cp.async kernel (profiles/r01), so group = 1 unless CHFSI_RASTER_GROUP
+  // (tuning only) says otherwise.
+  // TMA kernels: when the B panel (16 K N bytes) overflows L2, group row tiles so one
+  // resident wave covers `group` row tiles x all column tiles and the Y strips are
+  // re-read from L2: DRAM 115 -> 78 GB per c4 filter launch at identical speed
+  // (profiles/r01/raster.json); narrow blocks (Y resident in L2) keep group 1.
+  static const int env_group = [] {
+    const char* s = getenv("CHFSI_RASTER_GROUP");
+    return s ? std::max(1, atoi(s)) : 0;
+  }();
+  int group = 1;
+  if (g_table[c][opa][opb][epi].tma && 16.0 * (double)K * (double)N > 64e6) {
+    const long long resident = (long long)g_table[c][opa][opb][epi].occ * h->sm_count;
+    group = (int)std::max<long long>(1, resident / std::max(1, p.tiles_n));
+  }
+  if (env_group > 0) group = env_group;
+  p.group = std::max(1, std::min(group, p.tiles_m));
   const unsigned ntiles = (unsigned)((long long)p.tiles_m * p.tiles_n);
   if (pl.split == 1) {
     return run_kernel(h, c, g_table[c][opa][opb][epi], dim3(ntiles, 1, 1), p);
