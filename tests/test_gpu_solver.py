@@ -294,3 +294,22 @@ def test_generalized_baseline_recipe_sequence():
         lf = O.cholesky(s)
         ref = np.linalg.eigvalsh(O.reduce_standard(a, lf))[:40]
         assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-10
+
+
+def test_criterion7_report_csv_deterministic():
+    """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
+    non-timing report columns, eigenvalues and vectors."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.report import report_csv_text
+    rng = np.random.default_rng(9100)
+    evals = np.concatenate([np.sort(rng.uniform(0, 4, 8)), np.sort(rng.uniform(6, 10, 92))])
+    h = spectrum_matrix(rng, evals)
+    cfg = G.SolverConfig(nev=8)
+
+    def non_timing(rep):
+        return [",".join(ln.split(",")[:5]) for ln in report_csv_text(rep).splitlines()]
+
+    lam1, v1, r1 = G.chfsi_solve(h, None, cfg, seed=3)
+    lam2, v2, r2 = G.chfsi_solve(h, None, cfg, seed=3)
+    assert non_timing(r1) == non_timing(r2)
+    assert np.array_equal(lam1, lam2) and np.array_equal(v1.entries, v2.entries)

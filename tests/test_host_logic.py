@@ -141,6 +141,26 @@ def test_block_layout_roundtrip():
     assert back.flags.f_contiguous and np.array_equal(back, a)
 
 
+def test_report_csv_schema():
+    from paper_1305_5120_b200 import report as R
+    rep = G.SolveReport(n=10, nev=2)
+    rep.iterations.append(G.IterationStat(1, 3, 1, 1.5e-3, 2e-11, 63, 0.01, 0.002, 0.003, 0.0))
+    rep.iterations.append(G.IterationStat(2, 2, 2, 0.0, 0.0, 42, 0.01, 0.002, 0.003, 0.0))
+    txt = R.report_csv_text(rep)
+    lines = txt.strip().split("\n")
+    assert lines[0] == "iter,filtered_cols,converged,max_resid,matmul_count,t_filter,t_qr,t_rr,t_resid"
+    assert lines[1].startswith("1,3,1,1.500000e-03,63,")
+    rows = R.phase_rows(rep, total_seconds=0.1, config_hash="abc")
+    assert [r[0] for r in rows] == ["filter", "qr", "rayleigh_ritz", "residuals", "other"]
+    assert abs(sum(float(r[2]) for r in rows) - 1.0) < 1e-5
+    a = G.SequenceReport(mode="random", work=[10, 20], angles=[None, np.array([1e-3])])
+    b = G.SequenceReport(mode="reuse", work=[10, 10], angles=[None, np.array([1e-4])])
+    ratios = G.attach_work_ratios(a, b)
+    seq = R.sequence_csv_text(a, b, ratios).strip().split("\n")
+    assert seq[0] == "cycle,work_random,work_reuse,work_ratio,median_angle"
+    assert seq[1] == "1,10,10,," and seq[2] == "2,20,10,2.0000,1.000000e-04"
+
+
 def test_attach_work_ratios():
     a = G.SequenceReport(mode="random", work=[10, 20, 30])
     b = G.SequenceReport(mode="reuse", work=[10, 10, 10])
