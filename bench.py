@@ -316,6 +316,8 @@ def run_b200(args, rank, world, local_rank):
         line["sequence_c1"] = sequence_c1()
         line["c4_outer_iteration"] = c4_iteration_window()
         torch.cuda.empty_cache()
+        line["generalized_c4_setup"] = generalized_c4_setup()
+        torch.cuda.empty_cache()
         rate, sample, cores = cpu_filter_rate(n, m, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": sample}
@@ -370,6 +372,56 @@ def c4_iteration_window(n=20000, nev=2000, nex=200, degree=25):
                           "t_resid": it.t_resid, "filtered_cols": it.filtered_cols,
                           "locked": it.converged},
             "filter_share_of_iteration": it.t_filter / (it.t_filter + it.t_qr + it.t_rr + it.t_resid)}
+
+
+def generalized_c4_setup(n=20000):
+    """Per-problem generalized-to-standard cost at c4 scale (core.py:549-569): S = I +
+    0.1 B^H B / ||B^H B|| (norm from a 10-step Lanczos bound), zpotrf, blocked
+    triangular inverse, H = L^-1 A L^-H (two DMMA GEMMs), Hermitian check/symmetrise."""
+    import torch
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200 import workloads as Wl
+    dev = torch.device("cuda", torch.cuda.current_device())
+    eng = D.Engine.get(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    b = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+    s = torch.empty_like(b)
+    eng.zgemm("C", "N", n, n, n, 1.0, b, b, 0.0, s)  # B^H B (column-major blocks)
+    del b
+    eng.hermitize(s)
+    v0 = np.random.default_rng(4).standard_normal(n) + 0j
+    v0 /= np.linalg.norm(v0)
+    top, _, _ = eng.lanczos_bound(s, D.to_device(v0, dev), 10)
+    s.mul_(0.1 / top)
+    s.diagonal().add_(1.0)  # (k, n) block: the diagonal is the same set of entries
+    a, _ = Wl.spectrum_matrix_torch(5, n, dev)
+    t = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng.cholesky(s)
+    torch.cuda.synchronize()
+    t["potrf_s"] = time.perf_counter() - t0
+    linv = torch.empty_like(s)
+    t0 = time.perf_counter()
+    eng.trtri_lower(s, linv)
+    torch.cuda.synchronize()
+    t["trtri_s"] = time.perf_counter() - t0
+    w = torch.empty_like(s)
+    t0 = time.perf_counter()
+    eng.zgemm("N", "N", n, n, n, 1.0, linv, a, 0.0, w)
+    eng.zgemm("N", "C", n, n, n, 1.0, w, linv, 0.0, a)
+    torch.cuda.synchronize()
+    t["reduce_gemms_s"] = time.perf_counter() - t0
+    t["reduce_gemms_tflops"] = 2 * 8.0 * n ** 3 / t["reduce_gemms_s"] / 1e12
+    t0 = time.perf_counter()
+    fro, devn = eng.hermitian_norms(a)
+    eng.hermitize(a)
+    torch.cuda.synchronize()
+    t["hermitian_check_s"] = time.perf_counter() - t0
+    t["relative_hermitian_deviation"] = devn / fro
+    t["n"] = n
+    return t
 
 
 def measured_fp64_peaks(index):

@@ -296,6 +296,28 @@ def test_generalized_baseline_recipe_sequence():
         assert np.max(np.abs(lam - ref) / np.abs(ref)) <= 1e-10
 
 
+def test_reduction_at_scale_matches_oracle():
+    """reduce_to_standard / back_transform at n = 3000 (blocked recursive triangular
+    inverse: several recursion levels) against the oracle's LAPACK ztrsm route."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import spd_metric
+    n = 3000
+    rng = np.random.default_rng(31)
+    a = rand_hermitian(rng, n, scale=5.0)
+    s = spd_metric(rng, n)
+    lf_o = O.cholesky(s)
+    h_o = O.reduce_standard(a, lf_o)
+    lf = G.cholesky_factor(s)
+    assert np.linalg.norm(lf.entries - lf_o) <= 1e-13 * np.linalg.norm(lf_o)
+    h = G.reduce_to_standard(a, lf).entries
+    assert np.linalg.norm(h - h_o) <= 1e-12 * np.linalg.norm(h_o)
+    y = rng.standard_normal((n, 7)) + 1j * rng.standard_normal((n, 7))
+    c = G.back_transform(y, lf).entries
+    c_o = O.tri_solve(lf_o, y, side="left", adjoint=True)
+    assert np.linalg.norm(c - c_o) <= 1e-12 * np.linalg.norm(c_o)
+
+
 def test_criterion7_report_csv_deterministic():
     """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
     non-timing report columns, eigenvalues and vectors."""
