@@ -92,6 +92,18 @@ int chfsi_rayleigh_ritz(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H,
                         const void* d_Q, int64_t ldq, void* d_HQ, int64_t ldhq, void* d_Z,
                         int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w, double* h_res);
 
+/* Rayleigh-Ritz when the caller already holds HQ = H Q (column-sharded multi-GPU
+ * path: each rank computes H Q_p on its shard, then all-gathers HQ). */
+int chfsi_rayleigh_ritz_from_hq(chfsi_handle_t h, int64_t n, int64_t k, const void* d_Q,
+                                int64_t ldq, const void* d_HQ, int64_t ldhq, void* d_Z,
+                                int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w,
+                                double* h_res);
+
+/* F <- F - L (L^H F), twice (CGS2): the projection half of core.py:371-372. Column-local,
+ * so sharded callers run it on their own columns before the all-gather. */
+int chfsi_project_out(chfsi_handle_t h, int64_t n, int64_t k, void* d_F, int64_t ldf,
+                      const void* d_L, int64_t ldl, int64_t nl);
+
 /* r_j = ||HY_j - lam_j Y_j||_2, core.py:347-358 `residuals` and core.py:477. */
 int chfsi_residual_norms(chfsi_handle_t h, int64_t n, int64_t k, const void* d_HY, int64_t ldhy,
                          const void* d_Y, int64_t ldy, const double* h_lam, double* h_res);

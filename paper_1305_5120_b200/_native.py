@@ -51,6 +51,11 @@ SIGNATURES = {
     "chfsi_rayleigh_ritz": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                     _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64, _pdbl,
                                     _pdbl]),
+    "chfsi_rayleigh_ritz_from_hq": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p,
+                                            _i64, _c_void_p, _i64, _c_void_p, _i64, _pdbl,
+                                            _pdbl]),
+    "chfsi_project_out": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
+                                  _i64]),
     "chfsi_residual_norms": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                      _pdbl, _pdbl]),
     "chfsi_hermitian_norms": (_int, [_c_void_p, _i64, _c_void_p, _i64, _pdbl]),

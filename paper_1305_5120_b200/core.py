@@ -354,31 +354,35 @@ class DeviceSolver:
         self.n = hm.n
         self.sharded = None
         if group is not None:
-            from .distributed import ShardedFilter, world_info
+            from .distributed import ShardedPhases, world_info
             if world_info(group)[1] > 1:
-                self.sharded = ShardedFilter(group)
+                self.sharded = ShardedPhases(group)
 
     # -- phases -------------------------------------------------------
-    def _filter(self, active, out_other, a_edge, b_up, lam_ref):
+    def _filter(self, active, out_other, a_edge, b_up, lam_ref, locked=None):
         """Filter the active block in place (active is clobbered); returns the
         tensor with p_m(H) active: either ``active`` or ``out_other``. With a
-        process group, each rank filters its column shard and the shards are
-        all-gathered (distributed.ShardedFilter)."""
+        process group, each rank filters (and projects against ``locked``) its
+        column shard and the shards are all-gathered (distributed.ShardedPhases)."""
         if self.sharded is not None:
-            return self.sharded(self.eng, self.hb, active, out_other, self.cfg.degree, a_edge,
-                                b_up, lam_ref)
+            return self.sharded.filter_project(self.eng, self.hb, active, out_other,
+                                               self.cfg.degree, a_edge, b_up, lam_ref, locked)
         return self.eng.filter(self.hb, active, out_other, self.cfg.degree, a_edge, b_up, lam_ref)
 
-    def _orthonormalize(self, f, locked, t, q, rng):
-        """core.py:365-382 with rank-collapse replacement from the host RNG."""
+    def _orthonormalize(self, f, locked, t, q, rng, projected=False):
+        """core.py:365-382 with rank-collapse replacement from the host RNG.
+        ``projected``: f was already projected against ``locked`` (sharded path);
+        only a replaced column needs the projection again."""
         n = self.n
         for _ in range(dev.cols(f) + 2):
             try:
-                self.eng.orthonormalize(f, locked, t, q, rank_tol=1e-14)
+                self.eng.orthonormalize(f, None if projected else locked, t, q, rank_tol=1e-14)
                 return q
             except RankDeficient as exc:
                 col = rng.standard_normal(n) + 1j * rng.standard_normal(n)
                 f[exc.column].copy_(torch.from_numpy(col).to(self.device))
+                if projected and locked is not None:
+                    self.eng.project_out(f[exc.column:exc.column + 1], locked)
         raise RankDeficient(0)
 
     def _sync(self):
@@ -435,18 +439,24 @@ class DeviceSolver:
 
             # phase times from CUDA events on the solver stream: the iteration needs
             # only two host syncs (rank test after CholQR2; Ritz values + residuals)
+            locked = ws.locked[:nl] if nl else None
             ev[0].record(self.eng.stream)
-            f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref)
+            f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref, locked)
             ev[1].record(self.eng.stream)
             _count_products(cfg.degree * ncols)
             report.filter_flops += 8.0 * n * n * cfg.degree * ncols
 
-            q = self._orthonormalize(f, ws.locked[:nl] if nl else None, ws.hq[:ncols],
-                                     ws.fa[:ncols], rng)
+            q = self._orthonormalize(f, locked, ws.hq[:ncols], ws.fa[:ncols], rng,
+                                     projected=self.sharded is not None)
             ev[2].record(self.eng.stream)
 
-            w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
-                                            ws.hz[:ncols], residuals=True)
+            if self.sharded is not None:
+                self.sharded.hq(self.eng, self.hb, q, ws.hq[:ncols])
+                w, res = self.eng.rayleigh_ritz_from_hq(q, ws.hq[:ncols], ws.z[:ncols],
+                                                        ws.hz[:ncols])
+            else:
+                w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
+                                                ws.hz[:ncols], residuals=True)
             ev[3].record(self.eng.stream)
             _count_products(ncols)
             ev[3].synchronize()
@@ -562,14 +572,20 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None):
     bshape = (B.n, B.n) if bb is not None else bh.shape
     if tuple(ashape) != tuple(bshape):
         raise ContractViolation(f"A and B orders differ: {tuple(ashape)} vs {tuple(bshape)}")
-    lfac = cholesky_factor(B if bb is not None else bh)
+    cached = getattr(B, "_factor", None) if bb is not None else None
+    if cached is not None:
+        lfac, linv = cached
+    else:
+        lfac = cholesky_factor(B if bb is not None else bh)
+        linv = dev.empty(lfac.n, lfac.n, lfac.device_block().device)
+        engine(linv.device).trtri_lower(lfac.device_block(), linv)
+        if bb is not None:  # immutable B: keep (L, L^-1) for the next problem of a sequence
+            object.__setattr__(B, "_factor", (lfac, linv))
     d = lfac.device_block().device
     if ab is None:
         ab = dev.to_device(ah, d)
     n = dev.rows(ab)
     eng = engine(d)
-    linv = dev.empty(n, n, d)
-    eng.trtri_lower(lfac.device_block(), linv)
     hm = HermitianDenseMatrix(_reduce_block(ab, lfac, linv), rtol=1e-8)
     y0 = Y0
     if Y0 is not None and not (isinstance(Y0, str) and Y0 == "random"):

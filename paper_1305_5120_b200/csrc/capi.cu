@@ -67,7 +67,10 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
                    double* fro_out);
 int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long long ldh,
                   const double2* Q, long long ldq, double2* HQ, long long ldhq, double2* Z,
-                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host);
+                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host,
+                  bool hq_ready);
+int project_out(Handle* h, long long n, long long k, double2* F, long long ldf,
+                const double2* Lk, long long ldl, long long nl);
 
 // ---------------------------------------------------------------- peaks
 // Register-resident 4 x 4 block of independent 8x8 accumulators fed by 4 A and
@@ -283,7 +286,24 @@ int chfsi_rayleigh_ritz(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H,
   H_CHECK(h);
   if (k <= 0) return OK;
   return rayleigh_ritz(h, n, k, (const double2*)d_H, ldh, (const double2*)d_Q, ldq,
-                       (double2*)d_HQ, ldhq, (double2*)d_Z, ldz, (double2*)d_HZ, ldhz, h_w, h_res);
+                       (double2*)d_HQ, ldhq, (double2*)d_Z, ldz, (double2*)d_HZ, ldhz, h_w, h_res,
+                       false);
+}
+
+int chfsi_rayleigh_ritz_from_hq(chfsi_handle_t h, int64_t n, int64_t k, const void* d_Q,
+                                int64_t ldq, const void* d_HQ, int64_t ldhq, void* d_Z,
+                                int64_t ldz, void* d_HZ, int64_t ldhz, double* h_w,
+                                double* h_res) {
+  H_CHECK(h);
+  if (k <= 0) return OK;
+  return rayleigh_ritz(h, n, k, nullptr, 0, (const double2*)d_Q, ldq, (double2*)d_HQ, ldhq,
+                       (double2*)d_Z, ldz, (double2*)d_HZ, ldhz, h_w, h_res, true);
+}
+
+int chfsi_project_out(chfsi_handle_t h, int64_t n, int64_t k, void* d_F, int64_t ldf,
+                      const void* d_L, int64_t ldl, int64_t nl) {
+  H_CHECK(h);
+  return project_out(h, n, k, (double2*)d_F, ldf, (const double2*)d_L, ldl, nl);
 }
 
 int chfsi_residual_norms(chfsi_handle_t h, int64_t n, int64_t k, const void* d_HY, int64_t ldhy,

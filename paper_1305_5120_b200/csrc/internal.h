@@ -92,6 +92,10 @@ int gemm_override(int cfg, int split);
 int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
               int* cfg, int* split);
 
+// ---- solver phases (solver_ops.cu) ----
+int project_out(Handle* h, long long n, long long k, double2* F, long long ldf,
+                const double2* Lk, long long ldl, long long nl);
+
 // ---- misc kernels (kernels.cu) ----
 int residual_norms(Handle* h, long long n, long long k, const double2* HY, long long ldhy,
                    const double2* Y, long long ldy, const double* lam_dev, double* res_dev);

@@ -239,14 +239,7 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
                    double* fro_out) {
   *bad_col = -1;
   if (k <= 0) return OK;
-  if (nl > 0) {
-    double2* P = (double2*)scratch(h, SLOT_PROJ, (size_t)nl * k * sizeof(double2));
-    if (!P) return ERR_NOMEM;
-    for (int pass = 0; pass < 2; ++pass) {  // CGS2
-      CHFSI_TRY(zgemm(h, OP_C, OP_N, nl, k, n, ONE, Lk, ldl, F, ldf, ZERO, P, nl));
-      CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, nl, MONE, Lk, ldl, P, nl, ONE, F, ldf));
-    }
-  }
+  CHFSI_TRY(project_out(h, n, k, F, ldf, Lk, ldl, nl));  // CGS2 against the locked block
   double* vbase = (double*)scratch(h, SLOT_VEC, (size_t)(5 * k + 4) * sizeof(double));
   if (!vbase) return ERR_NOMEM;
   const OrthVec dv = orth_vec_layout(vbase, k);
@@ -298,18 +291,34 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
   return OK;
 }
 
+// CGS2 projection of F against the locked block L (first half of core.py:371-372);
+// column-local, so a column-sharded caller can run it on its own shard only.
+int project_out(Handle* h, long long n, long long k, double2* F, long long ldf,
+                const double2* Lk, long long ldl, long long nl) {
+  if (nl <= 0 || k <= 0) return OK;
+  double2* P = (double2*)scratch(h, SLOT_PROJ, (size_t)nl * k * sizeof(double2));
+  if (!P) return ERR_NOMEM;
+  for (int pass = 0; pass < 2; ++pass) {
+    CHFSI_TRY(zgemm(h, OP_C, OP_N, nl, k, n, ONE, Lk, ldl, F, ldf, ZERO, P, nl));
+    CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, nl, MONE, Lk, ldl, P, nl, ONE, F, ldf));
+  }
+  return OK;
+}
+
 // core.py:318-330 `_rr_raw` plus the residual norms of core.py:477, with a single
 // host sync: Ritz values, residuals and the zheevd info come back together.
+// hq_ready: the caller already holds HQ = H Q (column-sharded multi-GPU path).
 int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long long ldh,
                   const double2* Q, long long ldq, double2* HQ, long long ldhq, double2* Z,
-                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host) {
+                  long long ldz, double2* HZ, long long ldhz, double* w_host, double* res_host,
+                  bool hq_ready) {
   double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
   double* v = (double*)scratch(h, SLOT_VEC, (size_t)(2 * k + 2) * sizeof(double));
   if (!G || !v) return ERR_NOMEM;
   double* w_dev = v;
   double* r_dev = v + k;
   int* info_dev = reinterpret_cast<int*>(v + 2 * k);
-  CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, Q, ldq, ZERO, HQ, ldhq));
+  if (!hq_ready) CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, Q, ldq, ZERO, HQ, ldhq));
   CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, Q, ldq, HQ, ldhq, ZERO, G, k));
   CHFSI_TRY(hermitize(h, k, G, k));
   int lwork = 0;

@@ -177,6 +177,24 @@ class Engine:
                      res.ctypes.data_as(pd) if residuals else None)
         return (w, res) if residuals else w
 
+    def rayleigh_ritz_from_hq(self, Q, HQ, Z, HZ):
+        """Rayleigh-Ritz given HQ = H Q: (Ritz values, residual norms), one host sync."""
+        n, k = rows(Q), cols(Q)
+        w = np.empty(k, dtype=np.float64)
+        res = np.empty(k, dtype=np.float64)
+        pd = ctypes.POINTER(ctypes.c_double)
+        _native.call("chfsi_rayleigh_ritz_from_hq", self.h, n, k, ptr(Q), ld(Q), ptr(HQ), ld(HQ),
+                     ptr(Z), ld(Z), ptr(HZ), ld(HZ), w.ctypes.data_as(pd), res.ctypes.data_as(pd))
+        return w, res
+
+    def project_out(self, F, L):
+        """F <- F - L (L^H F), twice (CGS2); no-op when L is None."""
+        if L is None or cols(L) == 0 or cols(F) == 0:
+            return F
+        _native.call("chfsi_project_out", self.h, rows(F), cols(F), ptr(F), ld(F), ptr(L), ld(L),
+                     cols(L))
+        return F
+
     def residual_norms(self, HY, Y, lam):
         n, k = rows(Y), cols(Y)
         lam = np.ascontiguousarray(lam, dtype=np.float64)

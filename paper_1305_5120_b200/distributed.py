@@ -108,16 +108,19 @@ def all_gather_values(vals, shards, group=None):
     return out
 
 
-class ShardedFilter:
-    """Column-sharded Chebyshev filter for DeviceSolver.
+class ShardedPhases:
+    """Column-sharded phases of one outer iteration.
 
-    Each rank filters its contiguous column range of the active block (no
-    communication inside the filter: core.py:276-283 is column-separable),
-    then the shards are all-gathered so every rank holds the full filtered
-    block for CGS2/CholQR2 and Rayleigh-Ritz. Those later phases run
+    * ``filter_project``: each rank filters its contiguous column range of the
+      active block (core.py:276-283 is column-separable) and projects it
+      against the locked block (CGS2 is column-local too), then the shards are
+      all-gathered: every rank holds the full projected block.
+    * ``hq``: H Q_p on own columns, all-gathered into HQ (the n^2 k term of
+      Rayleigh-Ritz).
+    CholQR2, the k x k eigenproblem, Z = QW, HZ = HQ W and the residuals run
     redundantly on identical inputs with deterministic kernels, so every rank
-    reaches the same Ritz values, residuals and locking decision without any
-    further collective.
+    reaches the same Ritz values and locking decision with no further
+    collective. The only collectives are two all-gathers per iteration.
     """
 
     def __init__(self, group=None):
@@ -125,17 +128,30 @@ class ShardedFilter:
         self.rank, self.world = world_info(group)
         self._buf = None
 
-    def __call__(self, eng, H, active, other, degree, a, b, lam_ref):
-        k, n = active.shape[0], active.shape[1]
+    def _gather(self, sh, mine, out):
+        n = out.shape[1]
+        need = sh.padded * self.world
+        if self._buf is None or self._buf.shape[0] < need or self._buf.shape[1] != n:
+            self._buf = torch.empty((need, n), dtype=out.dtype, device=out.device)
+        gathered = self._buf[:need]
+        sh.all_gather(mine, gathered, self.group)
+        return sh.compact(gathered, out)
+
+    def filter_project(self, eng, H, active, other, degree, a, b, lam_ref, locked=None):
+        k = active.shape[0]
         sh = ColumnShards(k, self.world)
         lo, hi = sh.range(self.rank)
         if hi > lo:
             mine = eng.filter(H, active[lo:hi], other[lo:hi], degree, a, b, lam_ref)
+            eng.project_out(mine, locked)
         else:
             mine = active[lo:hi]
-        need = sh.padded * self.world
-        if self._buf is None or self._buf.shape[0] < need or self._buf.shape[1] != n:
-            self._buf = torch.empty((need, n), dtype=active.dtype, device=active.device)
-        gathered = self._buf[:need]
-        sh.all_gather(mine, gathered, self.group)
-        return sh.compact(gathered, other[:k])
+        return self._gather(sh, mine, other[:k])
+
+    def hq(self, eng, H, Q, HQ):
+        k, n = Q.shape[0], Q.shape[1]
+        sh = ColumnShards(k, self.world)
+        lo, hi = sh.range(self.rank)
+        if hi > lo:
+            eng.zgemm("N", "N", n, hi - lo, n, 1.0, H, Q[lo:hi], 0.0, HQ[lo:hi])
+        return self._gather(sh, HQ[lo:hi], HQ[:k])

@@ -123,10 +123,12 @@ class HermitianDenseMatrix(_DeviceBacked):
 
     Construction checks ||H - H^H||_F <= rtol ||H||_F and symmetrises
     (H <- (H + H^H)/2, real diagonal) -- on the GPU, where the matrix then
-    stays resident.
+    stays resident. As a metric B of solve_generalized it also caches its
+    Cholesky factor and the factor's inverse (the matrix is immutable), so a
+    sequence with a fixed B factorises once (BASELINE c2-c4).
     """
 
-    __slots__ = ("_host", "_dev", "n")
+    __slots__ = ("_host", "_dev", "n", "_factor")
 
     def __init__(self, entries, rtol=1e-13, device=None):
         if isinstance(entries, HermitianDenseMatrix):

@@ -298,3 +298,32 @@ def test_full_size_filter_on_exact_eigenvectors(eng):
     # FP64 budget: H = Q diag(lam) Q^H is exact only to ~1e-13 ||H|| at n = 20000, and
     # the normalised recurrence (|p| <= 1 on the spectrum) carries that forward
     assert max(errs) <= 1e-9, (errs, list(gain))
+
+
+def test_project_out_and_rr_from_hq(eng):
+    """The split entry points used by the column-sharded solver: CGS2 projection on a
+    column range equals projecting the full block; RR from a precomputed HQ equals RR."""
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(77)
+    n, k, nl = 600, 24, 50
+    L = np.linalg.qr(crand(rng, n, nl))[0]
+    F = crand(rng, n, k)
+    dL = D.to_device(L, eng.device)
+    full = D.to_device(F, eng.device)
+    eng.project_out(full, dL)
+    part = D.to_device(F, eng.device)
+    eng.project_out(part[5:17], dL)  # only columns 5..16
+    ref = F - L @ (L.conj().T @ F)
+    got_full, got_part = D.to_host(full), D.to_host(part)
+    assert np.linalg.norm(got_full - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.linalg.norm(got_part[:, 5:17] - ref[:, 5:17]) <= 1e-12 * np.linalg.norm(ref)
+    assert np.array_equal(got_part[:, :5], F[:, :5])
+    h = spectrum_matrix(rng, np.linspace(-2.0, 3.0, n))
+    q = np.linalg.qr(crand(rng, n, k))[0]
+    dH, dQ = D.to_device(h, eng.device), D.to_device(q, eng.device)
+    bufs = [D.zeros(n, k, eng.device) for _ in range(6)]
+    w1, r1 = eng.rayleigh_ritz(dH, dQ, bufs[0], bufs[1], bufs[2], residuals=True)
+    eng.zgemm("N", "N", n, k, n, 1.0, dH, dQ, 0.0, bufs[3])
+    w2, r2 = eng.rayleigh_ritz_from_hq(dQ, bufs[3], bufs[4], bufs[5])
+    assert np.array_equal(w1, w2) and np.array_equal(r1, r2)
+    assert np.array_equal(D.to_host(bufs[1]), D.to_host(bufs[4]))

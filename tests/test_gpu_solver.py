@@ -318,6 +318,63 @@ def test_reduction_at_scale_matches_oracle():
     assert np.linalg.norm(c - c_o) <= 1e-12 * np.linalg.norm(c_o)
 
 
+@pytest.mark.parametrize("n,nev,nex", [(2, 1, 1), (5, 1, 1), (9, 3, 6), (16, 4, 12), (33, 1, 2)])
+def test_edge_sizes_including_full_search_space(n, nev, nex):
+    """Tiny orders, nev = 1, and nev + buffer == n (the search block is the whole space)."""
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(n * 10 + nev)
+    evals = np.sort(rng.uniform(-3.0, 3.0, n))
+    h = spectrum_matrix(rng, evals)
+    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=8, max_outer_iters=500)
+    lam, vecs, rep = G.chfsi_solve(h, None, cfg, seed=1)
+    assert lam.shape == (nev,) and (vecs.n, vecs.s) == (n, nev)
+    assert np.max(np.abs(lam - evals[:nev])) <= 1e-9 * max(1.0, np.max(np.abs(evals)))
+    assert np.all(G.residuals(h, vecs, lam) < cfg.tol)
+
+
+def test_wrapper_inputs_and_device_start_block():
+    """HermitianDenseMatrix / VectorBlock inputs (device-resident) give the same answer as
+    raw ndarrays; a VectorBlock start block is used without a host round trip."""
+    import paper_1305_5120_b200 as G
+    h, _ = gapped_matrix(71, 120, 10)
+    hm = G.HermitianDenseMatrix(h)
+    cfg = G.SolverConfig(nev=10)
+    lam_a, v_a, _ = G.chfsi_solve(h, None, cfg, seed=2)
+    lam_b, v_b, _ = G.chfsi_solve(hm, None, cfg, seed=2)
+    assert np.max(np.abs(lam_a - lam_b)) <= 1e-12 * np.max(np.abs(lam_a))
+    s = cfg.nev + cfg.buffer_cols
+    y0 = G.VectorBlock(np.linalg.qr(np.random.default_rng(3).standard_normal((120, s)) + 0j)[0])
+    lam_c, _, _ = G.chfsi_solve(hm, y0, cfg, prior=(float(lam_a[0]), float(lam_a[-1]) + 0.5), seed=4)
+    assert np.max(np.abs(lam_c - lam_a)) <= 1e-9
+
+
+def test_reference_config_object_is_accepted():
+    """A config with the reference's field names (e.g. chfsi.core.SolverConfig) is accepted."""
+    import paper_1305_5120_b200 as G
+
+    class RefConfig:
+        nev, tol, max_outer_iters, degree, lanczos_steps, buffer = 6, 1e-10, 200, 20, 10, None
+        buffer_cols = 1
+
+    h, _ = gapped_matrix(72, 60, 6)
+    lam, v, rep = G.chfsi_solve(h, None, RefConfig(), seed=5)
+    assert len(lam) == 6 and rep.converged
+
+
+def test_generalized_fixed_metric_factor_is_cached():
+    """A HermitianDenseMatrix metric keeps (L, L^-1): the second solve reuses them."""
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(73)
+    a = rand_hermitian(rng, 80, scale=3.0)
+    s = G.HermitianDenseMatrix(rand_spd(rng, 80))
+    cfg = G.SolverConfig(nev=5)
+    lam1, c1, _ = G.solve_generalized(a, s, None, cfg, seed=1)
+    lf, linv = s._factor
+    lam2, c2, _ = G.solve_generalized(a, s, None, cfg, seed=1)
+    assert s._factor[0] is lf and s._factor[1] is linv
+    assert np.array_equal(lam1, lam2)
+
+
 def test_criterion7_report_csv_deterministic():
     """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
     non-timing report columns, eigenvalues and vectors."""
