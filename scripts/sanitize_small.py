@@ -1,0 +1,44 @@
+"""Small end-to-end workload for `compute-sanitizer --tool memcheck`: every GEMM
+config/split on ragged shapes (TMA zero-fill edges), the fused filter, CholQR2 with
+locked vectors, Rayleigh-Ritz, a small solve and a generalized solve."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_1305_5120_b200 as G  # noqa: E402
+from paper_1305_5120_b200 import _native, device as D  # noqa: E402
+
+eng = D.Engine.get(torch.device("cuda", 0))
+lib = _native.load()
+rng = np.random.default_rng(0)
+
+
+def crand(*s):
+    return rng.standard_normal(s) + 1j * rng.standard_normal(s)
+
+
+for cfg in range(10):
+    for split in (1, 2):
+        lib.chfsi_gemm_override(cfg, split)
+        for (m, n, k) in [(13, 5, 27), (70, 33, 9)]:
+            ops = [("N", "N")] if cfg >= 7 else [("N", "N"), ("C", "N"), ("N", "C")]
+            for opa, opb in ops:
+                A = crand(m, k) if opa == "N" else crand(k, m)
+                B = crand(k, n) if opb == "N" else crand(n, k)
+                C = D.to_device(crand(m, n), eng.device)
+                eng.zgemm(opa, opb, m, n, k, 1.0, D.to_device(A, eng.device),
+                          D.to_device(B, eng.device), 0.5, C)
+lib.chfsi_gemm_override(-1, 0)
+from paper_1305_5120_b200.workloads import baseline_matrix  # noqa: E402
+h, lam, _ = baseline_matrix(1, 120)
+lam_g, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=10, buffer=3, degree=8,
+                                                      max_outer_iters=2000), seed=1)
+a = crand(40, 40)
+a = (a + a.conj().T) / 2
+b = crand(40, 40)
+b = b.conj().T @ b + 40 * np.eye(40)
+G.solve_generalized(a, b, None, G.SolverConfig(nev=4), seed=2)
+torch.cuda.synchronize()
+print("sanitize workload done", rep.outer_iterations)
