@@ -389,7 +389,7 @@ class DeviceSolver:
         self.eng.synchronize()
 
     # -- driver -------------------------------------------------------
-    def run(self, Y0, prior, rng):
+    def run(self, Y0, prior, rng, callback=None):
         cfg = self.cfg
         n, nev = self.n, cfg.nev
         s_tot = nev + cfg.buffer_cols
@@ -485,6 +485,8 @@ class DeviceSolver:
             report.t_qr += tq
             report.t_rr += trr
             report.t_resid += tres
+            if callback is not None:
+                callback(report.iterations[-1])
 
             comb = np.sort(np.concatenate([locked_vals, w[kk:]]))
             lam_ref = float(comb[0])
@@ -522,13 +524,14 @@ class DeviceSolver:
         return vals, VectorBlock(out, orthonormal=True), report
 
 
-def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None):
+def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None, callback=None):
     """Run ChFSI on a standard Hermitian problem (core.py:385-546).
 
     Same signature, return types, report fields, RNG order and exceptions
     as the reference; arithmetic on the GPU. ``group`` (keyword-only, B200
     extension): a torch.distributed process group with one process per GPU;
     the filter columns are then sharded across its ranks (H replicated).
+    ``callback`` (keyword-only, B200 extension): called with each IterationStat.
     """
     config = _as_config(config)
     if isinstance(H, HermitianDenseMatrix):
@@ -556,10 +559,10 @@ def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None):
             raise ContractViolation(f"start block must be {n} x {s_tot}, got {y.shape}")
         y0 = y
     hm = _hermitian(H)
-    return DeviceSolver(hm, config, group=group).run(y0, prior, rng)
+    return DeviceSolver(hm, config, group=group).run(y0, prior, rng, callback)
 
 
-def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None):
+def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callback=None):
     """A c = lambda B c for the nev lowest pairs (core.py:549-569):
     B = L L^H (cuSOLVER zpotrf), H = L^-1 A L^-H (triangular inverse + DMMA
     GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors."""
@@ -593,7 +596,8 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None):
         fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
         eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd)
         y0 = VectorBlock(fwd)
-    lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed, group=group)
+    lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed, group=group,
+                                  callback=callback)
     c = dev.empty(n, yv.s, d)
     eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c)
     return lam, VectorBlock(c), report

@@ -91,10 +91,31 @@ def main():
             y0 = G.VectorBlock(torch.cat([prev.device_block(), D.to_device(pad, dev)], dim=0))
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        if smat is None:
-            lamc, vecs, rep = G.chfsi_solve(amat, y0, cfg, prior=prior, seed=solver_rng)
-        else:
-            lamc, vecs, rep = G.solve_generalized(amat, smat, y0, cfg, prior=prior, seed=solver_rng)
+        progress = open(args.out + f".p{ell}.progress", "w")
+
+        def log(it, t1=t1, progress=progress):
+            # streamed so a run cut by the call limit still reports how far it got
+            if it.iteration % 25 == 0 or it.iteration < 5:
+                progress.write(json.dumps({"it": it.iteration, "cols": it.filtered_cols,
+                                           "locked": it.converged, "max_res": it.max_resid,
+                                           "t": time.perf_counter() - t1}) + "\n")
+                progress.flush()
+
+        try:
+            if smat is None:
+                lamc, vecs, rep = G.chfsi_solve(amat, y0, cfg, prior=prior, seed=solver_rng,
+                                                callback=log)
+            else:
+                lamc, vecs, rep = G.solve_generalized(amat, smat, y0, cfg, prior=prior,
+                                                      seed=solver_rng, callback=log)
+        except G.NotConverged as exc:
+            rep = exc.report
+            results["problems"].append({
+                "problem": ell, "not_converged": True, "s": time.perf_counter() - t1,
+                "outer_iterations": rep.outer_iterations, "locked": len(exc.eigenvalues),
+                "t_filter": rep.t_filter, "filter_tflops": rep.filter_tflops})
+            print(json.dumps(results["problems"][-1]), flush=True)
+            break
         dt = time.perf_counter() - t1
         # verification on the device
         vb = vecs.device_block()
@@ -127,7 +148,7 @@ def main():
         running = rep.est_lam_next if running is None else min(running, rep.est_lam_next)
         prior = (rep.est_lam1, running)
         del hv
-    results["total_s"] = sum(p["s_per_solve"] for p in results["problems"])
+    results["total_s"] = sum(p.get("s_per_solve", p.get("s", 0.0)) for p in results["problems"])
     json.dump(results, open(args.out, "w"), indent=1)
     print(json.dumps({"total_s": results["total_s"]}))
 
