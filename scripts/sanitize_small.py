@@ -33,8 +33,9 @@ for cfg in range(10):
 lib.chfsi_gemm_override(-1, 0)
 from paper_1305_5120_b200.workloads import baseline_matrix  # noqa: E402
 h, lam, _ = baseline_matrix(1, 120)
-lam_g, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=10, buffer=3, degree=8,
-                                                      max_outer_iters=2000), seed=1)
+lam_g, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=10, buffer=6, degree=12,
+                                                      max_outer_iters=5000,
+                                                      interval="block_top"), seed=1)
 a = crand(40, 40)
 a = (a + a.conj().T) / 2
 b = crand(40, 40)
