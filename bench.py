@@ -285,6 +285,11 @@ def run_b200(args, rank, world, local_rank):
     achieved = launch_flops / avg_launch_s / 1e12
 
     kernel_name = plan_kernel_name(eng, n, kp)
+    e2e_multi = None
+    if world > 1 and not args.no_extras:
+        # every rank takes part (collectives inside); max over ranks
+        e2e_multi = e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up,
+                                    lam_ref, dev)
     if rank != 0:
         return
     peaks = measured_fp64_peaks(local_rank)
@@ -307,7 +312,9 @@ def run_b200(args, rank, world, local_rank):
                      "peaks": peaks},
         "setup_s": t_gen,
     }
-    if not args.no_extras:
+    if e2e_multi is not None:
+        line["e2e"] = e2e_multi
+    if world == 1 and not args.no_extras:
         def leg(key, fn):
             # an optional leg must never cost the headline line
             try:
@@ -452,6 +459,51 @@ def committed_traffic(n, k):
         return d.get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up, lam_ref, dev, steps=2):
+    """N-GPU e2e: every rank runs the public chebyshev_filter on its column shard from
+    pinned host H / Y (H2D inside), the filtered shards are all-gathered (NCCL), and
+    rank 0 copies the full filtered block back to the host. Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200 import device as D
+    n, k, m = args.n, args.k, args.degree
+    lo, hi = shards.range(rank)
+    h_pin = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    h_pin.copy_(H)
+    y_pin = torch.empty((hi - lo, n), dtype=torch.complex128, pin_memory=True)
+    y_pin.copy_(Yfull[lo:hi])
+    h_np, y_np = h_pin.numpy().T, y_pin.numpy().T
+    spec = G.FilterSpec(degree=m, a=a_edge, b=b_up, lam_ref=lam_ref)
+    gathered = torch.empty((shards.padded * world, n), dtype=torch.complex128, device=dev)
+    full = torch.empty((k, n), dtype=torch.complex128, device=dev)
+    d2h = 0
+
+    def one():
+        nonlocal d2h
+        out = G.chebyshev_filter(h_np, y_np, spec)
+        shards.all_gather(out.device_block(), gathered)
+        shards.compact(gathered, full)
+        if rank == 0:
+            d2h = D.to_host(full).nbytes
+
+    one()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    return {"value": 8.0 * n * n * k * m * steps / float(dt) / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": int(world * 16 * n * n + 16 * n * k),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "path": "per rank chebyshev_filter(H, Y_shard, FilterSpec) + NCCL all-gather; "
+                    "rank 0 VectorBlock -> host"}
 
 
 def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
