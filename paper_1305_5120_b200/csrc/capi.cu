@@ -197,6 +197,8 @@ int chfsi_destroy(chfsi_handle_t h) {
   if (!h) return OK;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
+  destroy_filter_graphs(h);
+  if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   for (int i = 0; i < 8; ++i)
     if (h->scratch[i]) cudaFree(h->scratch[i]);
   if (h->d_info) cudaFree(h->d_info);

@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 namespace chfsi {
 
@@ -19,6 +20,22 @@ enum Status : int {
   ERR_NOT_PD = -4,     // Cholesky pivot failure (detail = 1-based pivot)
   ERR_RANK = -5,       // rank collapse (detail = 0-based column)
   ERR_NOMEM = -6,
+};
+
+// One captured filter call (degree fused GEMM steps) for fixed buffers and shape.
+// The graph bakes in pointers, so the entry owns its split-K workspace and its
+// coefficient buffer; only the coefficients are rewritten before each replay.
+struct FilterGraph {
+  const void *H = nullptr, *Y = nullptr, *W = nullptr;
+  long long n = 0, k = 0, ldh = 0, ldy = 0, ldw = 0;
+  int degree = 0, force_cfg = -1, force_split = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  double2* ws = nullptr;
+  double* coef = nullptr;
+  int result_in_w = 0;
+  long long launches = 0;
+  unsigned long long last_use = 0;
 };
 
 struct Handle {
@@ -34,7 +51,16 @@ struct Handle {
   int sm_count = 148;
   // launch counter: kernels this library launched since the last reset
   long long launches = 0;
+  // CUDA-graph cache of filter calls (solver_ops.cu) and the split-K workspace
+  // override used while capturing one
+  std::vector<FilterGraph>* graphs = nullptr;
+  unsigned long long graph_tick = 0;
+  cudaStream_t capture_stream = nullptr;  // private: the legacy default stream cannot capture
+  double2* ws_override = nullptr;
+  size_t ws_override_bytes = 0;
 };
+
+void destroy_filter_graphs(Handle* h);
 
 // scratch slots
 enum Slot : int {
@@ -85,10 +111,14 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
 // C may alias Y0). A is M x M, Y1/Y0/C are M x N.
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,
-                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc);
+                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
+                      const double* coef_dev = nullptr);
+// split-K workspace bytes the filter step's plan needs (pre-sized before graph capture)
+size_t filter_step_workspace(Handle* h, long long M, long long N);
 
 // Tuning hooks: force a tile config (-1 = cost model) / split-K factor (0 = auto).
 int gemm_override(int cfg, int split);
+void gemm_overrides(int* cfg, int* split);
 int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
               int* cfg, int* split);
 

@@ -10,6 +10,8 @@
 //                   eigenproblem (replaces the numba Jacobi _jacobi.py:14-80).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -32,6 +34,14 @@ const double2 MONE = {-1.0, 0.0};
   } while (0)
 
 }  // namespace
+
+static int filter_issue(Handle* h, long long n, long long k, int degree, const double* coef,
+                        const double* coef_dev, const double2* H, long long ldh, double2* Y,
+                        long long ldy, double2* W, long long ldw, int* result_in_w);
+static int filter_graphed(Handle* h, long long n, long long k, int degree, const double* coef,
+                          const double2* H, long long ldh, double2* Y, long long ldy, double2* W,
+                          long long ldw, int* result_in_w);
+bool filter_graphs_enabled();
 
 int potrf_lower(Handle* h, long long n, double2* A, long long lda, int* info_host) {
   int lwork = 0;
@@ -75,28 +85,159 @@ int filter(Handle* h, long long n, long long k, int degree, double a, double b, 
     set_error("filter degree must be >= 1");
     return ERR_ARG;
   }
-  const double c = (a + b) / 2.0;
-  const double e = (b - a) / 2.0;
-  const double sigma1 = e / (lam_ref - c);
-  double sigma = sigma1;
-  // y1 = sigma1/e * H y - c*sigma1/e * y
-  CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, Y, ldy, sigma1 / e, -c * sigma1 / e, nullptr, 0,
-                              0.0, W, ldw));
+  // scaled three-term recurrence coefficients {alpha, beta, gamma} per degree step
+  std::vector<double> coef(3 * (size_t)degree);
+  {
+    const double c = (a + b) / 2.0;
+    const double e = (b - a) / 2.0;
+    const double sigma1 = e / (lam_ref - c);
+    double sigma = sigma1;
+    // y1 = sigma1/e * H y - c*sigma1/e * y
+    coef[0] = sigma1 / e;
+    coef[1] = -c * sigma1 / e;
+    coef[2] = 0.0;
+    for (int j = 1; j < degree; ++j) {
+      // y2 = scale*(H y1) - c*scale*y1 - sigma*sigma_new*y0, written over y0
+      const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+      const double scale = 2.0 * sigma_new / e;
+      coef[3 * j] = scale;
+      coef[3 * j + 1] = -c * scale;
+      coef[3 * j + 2] = -(sigma * sigma_new);
+      sigma = sigma_new;
+    }
+  }
+  if (filter_graphs_enabled())
+    return filter_graphed(h, n, k, degree, coef.data(), H, ldh, Y, ldy, W, ldw, result_in_w);
+  return filter_issue(h, n, k, degree, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, result_in_w);
+}
+
+// The degree fused steps; with coef_dev the epilogues read the coefficients from
+// device memory (graph capture), else from the launch arguments.
+static int filter_issue(Handle* h, long long n, long long k, int degree, const double* coef,
+                        const double* coef_dev, const double2* H, long long ldh, double2* Y,
+                        long long ldy, double2* W, long long ldw, int* result_in_w) {
+  CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, Y, ldy, coef[0], coef[1], nullptr, 0, 0.0, W, ldw,
+                              coef_dev));
   double2* prev = Y;
   long long ldp = ldy;
   double2* cur = W;
   long long ldc = ldw;
   for (int j = 1; j < degree; ++j) {
-    const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
-    const double scale = 2.0 * sigma_new / e;
-    // y2 = scale*(H y1) - c*scale*y1 - sigma*sigma_new*y0, written over y0
-    CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, scale, -c * scale, prev, ldp,
-                                -(sigma * sigma_new), prev, ldp));
+    CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, coef[3 * j], coef[3 * j + 1], prev, ldp,
+                                coef[3 * j + 2], prev, ldp, coef_dev ? coef_dev + 3 * j : nullptr));
     std::swap(prev, cur);
     std::swap(ldp, ldc);
-    sigma = sigma_new;
   }
   *result_in_w = (cur == W) ? 1 : 0;
+  return OK;
+}
+
+// Opt-in (CHFSI_FILTER_GRAPHS=1). Measured on B200 (scripts/graph_micro.py): a replay
+// saves 12 % of a filter call at n = 1000 (each fused step is ~23 us of GPU work, so
+// the calls are not launch-bound), while a c0 solve hits 115 distinct
+// (width, buffer) configurations whose capture + instantiate cost more than the
+// replays save (c0 filter time 1.07 s -> 2.82 s). Off by default.
+bool filter_graphs_enabled() {
+  static const bool on = [] {
+    const char* s = getenv("CHFSI_FILTER_GRAPHS");
+    return s && s[0] == '1';
+  }();
+  return on;
+}
+
+void destroy_filter_graphs(Handle* h) {
+  if (!h->graphs) return;
+  for (auto& g : *h->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    if (g.ws) cudaFree(g.ws);
+    if (g.coef) cudaFree(g.coef);
+  }
+  delete h->graphs;
+  h->graphs = nullptr;
+}
+
+// CUDA-graph path: one captured launch sequence per (buffers, shape, degree); each
+// call only uploads the 3*degree coefficients and replays it. Small solves are
+// launch-bound (a fused step at n = 1000 is a few microseconds of GPU work).
+static int filter_graphed(Handle* h, long long n, long long k, int degree, const double* coef,
+                          const double2* H, long long ldh, double2* Y, long long ldy, double2* W,
+                          long long ldw, int* result_in_w) {
+  constexpr size_t kMaxGraphs = 32;
+  if (!h->graphs) h->graphs = new std::vector<FilterGraph>();
+  int fcfg = -1, fsplit = 0;
+  gemm_overrides(&fcfg, &fsplit);
+  FilterGraph* hit = nullptr;
+  for (auto& g : *h->graphs)
+    if (g.H == H && g.Y == Y && g.W == W && g.n == n && g.k == k && g.ldh == ldh &&
+        g.ldy == ldy && g.ldw == ldw && g.degree == degree && g.force_cfg == fcfg &&
+        g.force_split == fsplit) {
+      hit = &g;
+      break;
+    }
+  if (!hit) {
+    if (h->graphs->size() >= kMaxGraphs) {  // evict the least recently used entry
+      auto lru = h->graphs->begin();
+      for (auto it = h->graphs->begin(); it != h->graphs->end(); ++it)
+        if (it->last_use < lru->last_use) lru = it;
+      CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+      cudaGraphExecDestroy(lru->exec);
+      cudaGraphDestroy(lru->graph);
+      if (lru->ws) cudaFree(lru->ws);
+      cudaFree(lru->coef);
+      h->graphs->erase(lru);
+    }
+    FilterGraph g;
+    g.H = H; g.Y = Y; g.W = W;
+    g.n = n; g.k = k; g.ldh = ldh; g.ldy = ldy; g.ldw = ldw;
+    g.degree = degree; g.force_cfg = fcfg; g.force_split = fsplit;
+    const size_t ws_bytes = filter_step_workspace(h, n, k);  // also builds the kernel table
+    if (ws_bytes) CHFSI_CUDA(cudaMalloc(&g.ws, ws_bytes));
+    CHFSI_CUDA(cudaMalloc(&g.coef, 3 * (size_t)degree * sizeof(double)));
+    h->ws_override = g.ws;
+    h->ws_override_bytes = ws_bytes;
+    const long long before = h->launches;
+    // capture on a private stream (capture executes nothing; the caller's stream may be
+    // the legacy default stream, which cannot capture), replay on the caller's stream
+    if (!h->capture_stream)
+      CHFSI_CUDA(cudaStreamCreateWithFlags(&h->capture_stream, cudaStreamNonBlocking));
+    cudaStream_t user_stream = h->stream;
+    h->stream = h->capture_stream;
+    cudaError_t ce = cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal);
+    int st = OK;
+    cudaGraph_t graph = nullptr;
+    if (ce == cudaSuccess) {
+      st = filter_issue(h, n, k, degree, coef, g.coef, H, ldh, Y, ldy, W, ldw, &g.result_in_w);
+      ce = cudaStreamEndCapture(h->stream, &graph);
+    }
+    h->stream = user_stream;
+    h->ws_override = nullptr;
+    h->ws_override_bytes = 0;
+    if (st != OK || ce != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      if (g.ws) cudaFree(g.ws);
+      cudaFree(g.coef);
+      if (st != OK) return st;
+      set_error(std::string("filter graph capture: ") + cudaGetErrorString(ce));
+      return ERR_CUDA;
+    }
+    g.launches = h->launches - before;
+    h->launches = before;  // captured, not executed
+    static const bool dbg = getenv("CHFSI_GRAPH_DEBUG") != nullptr;
+    if (dbg)
+      fprintf(stderr, "[chfsi] filter graph capture #%zu: n=%lld k=%lld degree=%d Y=%p W=%p\n",
+              h->graphs->size() + 1, n, k, degree, (const void*)Y, (const void*)W);
+    g.graph = graph;
+    CHFSI_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+    h->graphs->push_back(g);
+    hit = &h->graphs->back();
+  }
+  hit->last_use = ++h->graph_tick;
+  CHFSI_CUDA(cudaMemcpyAsync(hit->coef, coef, 3 * (size_t)degree * sizeof(double),
+                             cudaMemcpyHostToDevice, h->stream));
+  CHFSI_CUDA(cudaGraphLaunch(hit->exec, h->stream));
+  h->launches += hit->launches;
+  *result_in_w = hit->result_in_w;
   return OK;
 }
 

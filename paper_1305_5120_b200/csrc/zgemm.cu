@@ -23,7 +23,13 @@ namespace chfsi {
 __global__ void zgemm_splitk_reduce_kernel(int M, int N, int S, const double2* __restrict__ ws,
                                            int epi, double2 alpha, double2 beta, double2* C,
                                            long long ldc, const double2* Y1, long long ld1,
-                                           const double2* Y0, long long ld0, double gamma) {
+                                           const double2* Y0, long long ld0, double gamma,
+                                           const double* coef) {
+  if (coef != nullptr) {  // graph-replayed filter step: coefficients live on the device
+    alpha.x = coef[0];
+    beta.x = coef[1];
+    gamma = coef[2];
+  }
   const long long total = (long long)M * N;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -204,7 +210,7 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
     const long long tn = (N + kBN[c] - 1) / kBN[c];
     const long long tiles = tm * tn;
     const long long ktiles = std::max<long long>(1, (K + bk - 1) / bk);
-    int max_split = (int)std::min<long long>(64, ktiles / (128 / bk));
+    int max_split = (int)std::min<long long>(64, ktiles / (32 / bk));
     if (M * N * 16LL * 8 > (2LL << 30)) max_split = 1;  // cap workspace
     int s_lo = 1, s_hi = std::max(1, max_split);
     if (g_force_split > 0) s_lo = s_hi = g_force_split;
@@ -353,7 +359,10 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
     return run_kernel(h, c, g_table[c][opa][opb][epi], dim3(ntiles, 1, 1), p);
   }
   const size_t ws_bytes = (size_t)pl.split * M * N * sizeof(double2);
-  double2* ws = (double2*)scratch(h, SLOT_SPLITK, ws_bytes);
+  // while a filter graph is being captured, partials go to the graph's own workspace
+  double2* ws = (h->ws_override && h->ws_override_bytes >= ws_bytes)
+                    ? h->ws_override
+                    : (double2*)scratch(h, SLOT_SPLITK, ws_bytes);
   if (!ws) return ERR_NOMEM;
   GemmParams q = p;
   q.k_chunk = pl.k_chunk;
@@ -365,7 +374,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);
   zgemm_splitk_reduce_kernel<<<blocks, threads, 0, h->stream>>>(
       (int)M, (int)N, pl.split, ws, epi, p.alpha, p.beta, p.C, p.ldc, p.B, p.ldb, p.Y0, p.ld0,
-      p.gamma);
+      p.gamma, epi == EPI_FILTER ? p.coef : nullptr);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;
@@ -381,6 +390,11 @@ int gemm_override(int cfg, int split) {
   g_force_cfg = cfg;
   g_force_split = split;
   return OK;
+}
+
+void gemm_overrides(int* cfg, int* split) {
+  *cfg = g_force_cfg;
+  *split = g_force_split;
 }
 
 int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
@@ -410,7 +424,8 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
 
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,
-                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc) {
+                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
+                      const double* coef_dev) {
   GemmParams p{};
   p.A = A; p.lda = lda;
   p.B = Y1; p.ldb = ld1;
@@ -418,7 +433,14 @@ int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, lon
   p.alpha = make_double2(alpha, 0.0);
   p.beta = make_double2(beta, 0.0);
   p.Y0 = Y0; p.ld0 = ld0; p.gamma = gamma;
+  p.coef = coef_dev;
   return launch(h, OP_N, OP_N, EPI_FILTER, M, N, M, p);
+}
+
+size_t filter_step_workspace(Handle* h, long long M, long long N) {
+  if (ensure_table() != OK) return 0;
+  const Plan pl = cached_plan(h, OP_N, OP_N, EPI_FILTER, M, N, M);
+  return pl.split > 1 ? (size_t)pl.split * M * N * sizeof(double2) : 0;
 }
 
 }  // namespace chfsi

@@ -40,7 +40,23 @@ struct GemmParams {
   // grouped raster: blockIdx.x enumerates tiles so that `group` consecutive row tiles
   // share each column tile inside one wave (Y strips are reused from L2)
   int tiles_m, tiles_n, group;
+  // EPI_FILTER: when non-null, {alpha, beta, gamma} are read from device memory
+  // (CUDA-graph replays of the filter reuse one captured launch sequence while the
+  // Chebyshev coefficients change every outer iteration)
+  const double* coef;
 };
+
+__device__ __forceinline__ void filter_coef(const GemmParams& p, double& a, double& b, double& g) {
+  if (p.coef != nullptr) {
+    a = p.coef[0];
+    b = p.coef[1];
+    g = p.coef[2];
+  } else {
+    a = p.alpha.x;
+    b = p.beta.x;
+    g = p.gamma;
+  }
+}
 
 // linear tile id -> (row tile, column tile), grouped raster
 __device__ __forceinline__ void tile_coords(const GemmParams& p, int b, int& mi, int& ni) {
@@ -197,13 +213,15 @@ zgemm_dmma_kernel(const GemmParams p) {
           p.ws[(long long)blockIdx.z * p.M * p.N + m + (long long)n * p.M] = make_double2(xr, xi);
         } else if (EPI == EPI_FILTER) {
           // out = alpha*acc + beta*Y1 + gamma*Y0 with real coefficients
+          double fa, fb, fg;
+          filter_coef(p, fa, fb, fg);
           const double2 y1 = p.B[m + (long long)n * p.ldb];
-          double orr = p.alpha.x * xr + p.beta.x * y1.x;
-          double oi = p.alpha.x * xi + p.beta.x * y1.y;
+          double orr = fa * xr + fb * y1.x;
+          double oi = fa * xi + fb * y1.y;
           if (p.Y0 != nullptr) {
             const double2 y0 = p.Y0[m + (long long)n * p.ld0];
-            orr += p.gamma * y0.x;
-            oi += p.gamma * y0.y;
+            orr += fg * y0.x;
+            oi += fg * y0.y;
           }
           p.C[m + (long long)n * p.ldc] = make_double2(orr, oi);
         } else {

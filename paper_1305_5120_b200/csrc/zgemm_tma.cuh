@@ -287,13 +287,15 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         if (EPI == EPI_PARTIAL) {
           p.ws[(long long)blockIdx.z * p.M * p.N + m + (long long)n * p.M] = make_double2(xr, xi);
         } else if (EPI == EPI_FILTER) {
+          double fa, fb, fg;
+          filter_coef(p, fa, fb, fg);
           const double2 y1 = p.B[m + (long long)n * p.ldb];
-          double orr = p.alpha.x * xr + p.beta.x * y1.x;
-          double oi = p.alpha.x * xi + p.beta.x * y1.y;
+          double orr = fa * xr + fb * y1.x;
+          double oi = fa * xi + fb * y1.y;
           if (p.Y0 != nullptr) {
             const double2 y0 = p.Y0[m + (long long)n * p.ld0];
-            orr += p.gamma * y0.x;
-            oi += p.gamma * y0.y;
+            orr += fg * y0.x;
+            oi += fg * y0.y;
           }
           p.C[m + (long long)n * p.ldc] = make_double2(orr, oi);
         } else {
