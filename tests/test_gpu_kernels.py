@@ -300,6 +300,23 @@ def test_full_size_filter_on_exact_eigenvectors(eng):
     assert max(errs) <= 1e-9, (errs, list(gain))
 
 
+def test_shifted_cholqr3_on_ill_conditioned_block(eng):
+    """cond(F) ~ 1e10: Cholesky of F^H F (cond ~ 1e20) breaks down, the shifted CholQR3
+    path (Fukaya et al.) must still return an orthonormal basis of range(F)."""
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(5)
+    n, k = 400, 12
+    U = np.linalg.qr(crand(rng, n, k))[0]
+    V = np.linalg.qr(crand(rng, k, k))[0]
+    F = (U * np.logspace(0, -10, k)) @ V  # singular values 1 .. 1e-10
+    dF = D.to_device(F, eng.device)
+    dT, dQ = D.zeros(n, k, eng.device), D.zeros(n, k, eng.device)
+    eng.orthonormalize(dF, None, dT, dQ)
+    Q = D.to_host(dQ)
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(k)) <= 1e-12 * np.sqrt(k)
+    assert np.linalg.norm(U - Q @ (Q.conj().T @ U)) <= 1e-6  # same span (up to cond * eps)
+
+
 def test_project_out_and_rr_from_hq(eng):
     """The split entry points used by the column-sharded solver: CGS2 projection on a
     column range equals projecting the full block; RR from a precomputed HQ equals RR."""

@@ -375,6 +375,24 @@ def test_generalized_fixed_metric_factor_is_cached():
     assert np.array_equal(lam1, lam2)
 
 
+def test_rank_collapse_in_start_block_is_replaced_like_the_reference():
+    """Duplicate start columns make the bootstrap QR rank-deficient; like core.py:375-381
+    the collapsed column is replaced by a fresh random vector from the solver's
+    Generator, and the solve converges to the oracle's (same replacement semantics)."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    h, evals = gapped_matrix(81, 100, 8)
+    cfg = G.SolverConfig(nev=8, buffer=3, max_outer_iters=300)
+    rng0 = np.random.default_rng(3)
+    y0 = rng0.standard_normal((100, 11)) + 1j * rng0.standard_normal((100, 11))
+    y0[:, 5] = y0[:, 2]
+    lam, v, rep = G.chfsi_solve(h, y0, cfg, seed=4)
+    lam_o, v_o, _ = O.solve(h, y0, 8, 3, cfg.degree, cfg.tol, 300, seed=4)
+    assert np.max(np.abs(lam - lam_o) / np.abs(lam_o)) <= 1e-10
+    assert np.max(np.abs(lam - evals[:8]) / np.abs(evals[:8])) <= 1e-10
+    assert _angle(v.entries, v_o) < 1e-8
+
+
 def test_criterion7_report_csv_deterministic():
     """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
     non-timing report columns, eigenvalues and vectors."""
