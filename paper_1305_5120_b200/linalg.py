@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 from . import device as dev
-from .errors import ContractViolation, DimensionMismatch, RankDeficient
+from .errors import ContractViolation, DimensionMismatch, OracleNoConvergence, RankDeficient
 
 __all__ = [
     "HermitianDenseMatrix", "VectorBlock", "LowerTriangularFactor", "gemm",
@@ -340,6 +340,15 @@ def oracle_eig(H, max_sweeps=30):
         if h.ndim != 2 or h.shape[0] != h.shape[1]:
             raise ContractViolation(f"expected a square matrix, got shape {h.shape}")
         block = dev.to_device(h, default_device())
+    if max_sweeps < 1 and dev.rows(block) > 1:
+        # the reference's Jacobi with no sweep budget converges only if the input is
+        # already diagonal to 1e-13 ||H||_F (_jacobi.py:21-28, linalg.py:312-318)
+        fro = float(torch.linalg.vector_norm(block))
+        off = float(torch.linalg.vector_norm(block - torch.diag_embed(torch.diagonal(block))))
+        if fro > 0 and off > 1e-13 * fro:
+            raise OracleNoConvergence(
+                f"eigensolver: off-diagonal norm {off:.3e} above tolerance with a zero sweep "
+                f"budget (n={dev.rows(block)})")
     w = engine(block.device).heevd(block)
     return w, VectorBlock(block)
 

@@ -393,6 +393,50 @@ def test_rank_collapse_in_start_block_is_replaced_like_the_reference():
     assert _angle(v.entries, v_o) < 1e-8
 
 
+def test_linalg_dropin_semantics():
+    """Reference test_linalg.py behaviours on the GPU-backed linalg layer."""
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(15)
+    h = rand_hermitian(rng, 8)
+    with pytest.raises(G.OracleNoConvergence):
+        G.oracle_eig(h, max_sweeps=0)
+    lam, v = G.oracle_eig(np.diag([3.0, 1.0, 2.0]).astype(complex))
+    assert np.array_equal(lam, [1.0, 2.0, 3.0])
+    assert np.allclose(np.abs(v.entries), np.eye(3)[:, [1, 2, 0]], atol=1e-14)
+    lam, _ = G.oracle_eig(np.array([[2.0, 1.0 - 1j], [1.0 + 1j, 3.0]]))
+    assert np.allclose(lam, [1.0, 4.0], atol=1e-14)
+    # gemm: alpha = 0 keeps C and counts nothing; square A counted; vector operand
+    G.reset_product_count()
+    x = rng.standard_normal((4, 3)) + 1j * rng.standard_normal((4, 3))
+    out = G.gemm(0.0, np.eye(4, dtype=complex), x, beta=1.0, c=x)
+    assert np.array_equal(out, x) and G.product_count() == 0
+    sq = rng.standard_normal((6, 6)) + 0j
+    blk = rng.standard_normal((6, 3)) + 0j
+    G.gemm(1.0, sq, blk)
+    assert G.product_count() == 3
+    G.gemm(1.0, rng.standard_normal((4, 6)) + 0j, blk)
+    assert G.product_count() == 3
+    v5 = rng.standard_normal(5) + 1j * rng.standard_normal(5)
+    a5 = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5))
+    assert G.gemm(1.0, a5, v5).shape == (5,)
+    assert np.allclose(G.gemm(1.0, a5, v5), a5 @ v5, rtol=1e-14, atol=0)
+    with pytest.raises(G.DimensionMismatch):
+        G.gemm(1.0, np.ones((3, 4), dtype=complex), np.ones((3, 2), dtype=complex))
+    with pytest.raises(G.ContractViolation):
+        G.gemm(1.0, np.eye(2, dtype=complex), np.eye(2, dtype=complex), beta=1.0)
+    # QR rank collapse names the column; Cholesky pivot is 1-based
+    y = rng.standard_normal((10, 3)) + 1j * rng.standard_normal((10, 3))
+    y[:, 2] = y[:, 0]
+    with pytest.raises(G.RankDeficient) as exc:
+        G.householder_qr(y)
+    assert exc.value.column == 2
+    with pytest.raises(G.NotPositiveDefinite) as exc:
+        G.cholesky_factor(np.diag([1.0, -1.0]).astype(complex))
+    assert exc.value.pivot == 2
+    lf = G.cholesky_factor(np.diag([4.0, 9.0]).astype(complex))
+    assert np.array_equal(lf.entries, np.diag([2.0, 3.0]).astype(complex))
+
+
 def test_criterion7_report_csv_deterministic():
     """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
     non-timing report columns, eigenvalues and vectors."""
