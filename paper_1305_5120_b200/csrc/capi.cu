@@ -199,7 +199,7 @@ int chfsi_destroy(chfsi_handle_t h) {
   cudaStreamSynchronize(h->stream);
   destroy_filter_graphs(h);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < Handle::kSlots; ++i)
     if (h->scratch[i]) cudaFree(h->scratch[i]);
   if (h->d_info) cudaFree(h->d_info);
   if (h->h_pinned) cudaFreeHost(h->h_pinned);

@@ -43,8 +43,9 @@ struct Handle {
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   // grow-only scratch arenas (stream-ordered reuse is safe: one stream)
-  void* scratch[8] = {nullptr};
-  size_t scratch_bytes[8] = {0};
+  static constexpr int kSlots = 9;
+  void* scratch[kSlots] = {nullptr};
+  size_t scratch_bytes[kSlots] = {0};
   int* d_info = nullptr;
   double* h_pinned = nullptr;   // small pinned host staging
   size_t h_pinned_bytes = 0;
@@ -72,6 +73,7 @@ enum Slot : int {
   SLOT_VEC = 5,     // small vectors (eigvalues, diagonals, norms)
   SLOT_TRI = 6,     // triangular-inverse temporaries
   SLOT_LANCZOS = 7, // Lanczos basis
+  SLOT_COLRED = 8,  // per-column partial sums (split column reductions)
 };
 
 void set_error(const std::string& msg);

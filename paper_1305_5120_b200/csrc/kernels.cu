@@ -53,6 +53,82 @@ __global__ void zdotc_cols_kernel(long long n, const double2* __restrict__ X, lo
   if (threadIdx.x == 0) out[j] = make_double2(sr, si);
 }
 
+// Narrow blocks (the tail of a solve: k ~ 200 columns) give one CTA per column too few
+// CTAs to saturate HBM, so columns are split into S row chunks; partial sums land in
+// partial[j*S + s] and a second kernel adds them in fixed s order (deterministic).
+__global__ void residual_partial_kernel(long long n, int S, const double2* __restrict__ HY,
+                                        long long ldhy, const double2* __restrict__ Y,
+                                        long long ldy, const double* __restrict__ lam,
+                                        double* __restrict__ partial) {
+  __shared__ double red[RT / 32];
+  const long long j = blockIdx.x;
+  const int s = blockIdx.y;
+  const long long chunk = (n + S - 1) / S;
+  const long long i0 = s * chunk, i1 = min(n, i0 + chunk);
+  const double l = lam[j];
+  const double2* hy = HY + j * ldhy;
+  const double2* y = Y + j * ldy;
+  double acc = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += RT) {
+    const double2 a = hy[i], b = y[i];
+    const double rr = a.x - l * b.x, ri = a.y - l * b.y;
+    acc += rr * rr + ri * ri;
+  }
+  acc = block_sum<RT>(acc, red);
+  if (threadIdx.x == 0) partial[j * S + s] = acc;
+}
+
+__global__ void zdotc_partial_kernel(long long n, int S, const double2* __restrict__ X,
+                                     long long ldx, const double2* __restrict__ Y, long long ldy,
+                                     double2* __restrict__ partial) {
+  __shared__ double red[RT / 32];
+  const long long j = blockIdx.x;
+  const int s = blockIdx.y;
+  const long long chunk = (n + S - 1) / S;
+  const long long i0 = s * chunk, i1 = min(n, i0 + chunk);
+  const double2* x = X + j * ldx;
+  const double2* y = Y + j * ldy;
+  double sr = 0.0, si = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += RT) {
+    const double2 a = x[i], b = y[i];
+    sr += a.x * b.x + a.y * b.y;
+    si += a.x * b.y - a.y * b.x;
+  }
+  sr = block_sum<RT>(sr, red);
+  si = block_sum<RT>(si, red);
+  if (threadIdx.x == 0) partial[j * S + s] = make_double2(sr, si);
+}
+
+__global__ void finish_sqrt_kernel(long long k, int S, const double* __restrict__ partial,
+                                   double* __restrict__ out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double s = 0.0;
+  for (int t = 0; t < S; ++t) s += partial[j * S + t];
+  out[j] = sqrt(s);
+}
+
+__global__ void finish_sum2_kernel(long long k, int S, const double2* __restrict__ partial,
+                                   double2* __restrict__ out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double sr = 0.0, si = 0.0;
+  for (int t = 0; t < S; ++t) {
+    sr += partial[j * S + t].x;
+    si += partial[j * S + t].y;
+  }
+  out[j] = make_double2(sr, si);
+}
+
+// row chunks per column so that k * S CTAs cover >= ~8 CTAs per SM (1 when k is wide)
+inline int column_splits(long long n, long long k) {
+  const long long want = 148LL * 8;
+  if (k >= want) return 1;
+  long long s = (want + k - 1) / k;
+  s = std::min<long long>(s, std::max<long long>(1, n / 2048));  // >= 2048 rows per chunk
+  return (int)std::max<long long>(1, std::min<long long>(s, 64));
+}
+
 constexpr int TS = 32;  // tile for transpose-type kernels
 
 // partials[2*(by*gx+bx)+{0,1}] = (sum |A_ij|^2, sum |A_ij - conj(A_ji)|^2) over tile (bx,by)
@@ -220,8 +296,20 @@ inline int grid_for(long long total, int threads = 256) {
 int residual_norms(Handle* h, long long n, long long k, const double2* HY, long long ldhy,
                    const double2* Y, long long ldy, const double* lam_dev, double* res_dev) {
   if (k <= 0) return OK;
-  residual_norms_kernel<<<(unsigned)k, RT, 0, h->stream>>>(n, HY, ldhy, Y, ldy, lam_dev, res_dev);
-  h->launches++;
+  const int S = column_splits(n, k);
+  if (S == 1) {
+    residual_norms_kernel<<<(unsigned)k, RT, 0, h->stream>>>(n, HY, ldhy, Y, ldy, lam_dev,
+                                                             res_dev);
+    h->launches++;
+    CHFSI_CHECK_LAUNCH();
+    return OK;
+  }
+  double* part = (double*)scratch(h, SLOT_COLRED, (size_t)k * S * sizeof(double));
+  if (!part) return ERR_NOMEM;
+  residual_partial_kernel<<<dim3((unsigned)k, (unsigned)S), RT, 0, h->stream>>>(
+      n, S, HY, ldhy, Y, ldy, lam_dev, part);
+  finish_sqrt_kernel<<<(unsigned)((k + 255) / 256), 256, 0, h->stream>>>(k, S, part, res_dev);
+  h->launches += 2;
   CHFSI_CHECK_LAUNCH();
   return OK;
 }
@@ -229,8 +317,19 @@ int residual_norms(Handle* h, long long n, long long k, const double2* HY, long 
 int zdotc_cols(Handle* h, long long n, long long k, const double2* X, long long ldx,
                const double2* Y, long long ldy, double2* out_dev) {
   if (k <= 0) return OK;
-  zdotc_cols_kernel<<<(unsigned)k, RT, 0, h->stream>>>(n, X, ldx, Y, ldy, out_dev);
-  h->launches++;
+  const int S = column_splits(n, k);
+  if (S == 1) {
+    zdotc_cols_kernel<<<(unsigned)k, RT, 0, h->stream>>>(n, X, ldx, Y, ldy, out_dev);
+    h->launches++;
+    CHFSI_CHECK_LAUNCH();
+    return OK;
+  }
+  double2* part = (double2*)scratch(h, SLOT_COLRED, (size_t)k * S * sizeof(double2));
+  if (!part) return ERR_NOMEM;
+  zdotc_partial_kernel<<<dim3((unsigned)k, (unsigned)S), RT, 0, h->stream>>>(n, S, X, ldx, Y,
+                                                                           ldy, part);
+  finish_sum2_kernel<<<(unsigned)((k + 255) / 256), 256, 0, h->stream>>>(k, S, part, out_dev);
+  h->launches += 2;
   CHFSI_CHECK_LAUNCH();
   return OK;
 }
