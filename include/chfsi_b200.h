@@ -61,6 +61,19 @@ int chfsi_filter(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a, d
                  double lam_ref, const void* d_H, int64_t ldh, void* d_Y, int64_t ldy,
                  void* d_W, int64_t ldw, int* h_result_in_w);
 
+/* The same filter when H arrives from HOST memory, core.py:287-311
+ * `chebyshev_filter(H, Y, spec)` called with an ndarray H (core.py:304 `_asarray`).
+ * h_H (column-major, leading dimension ldh_host >= n) is uploaded into d_H in
+ * `panels` row panels (0 = automatic) on a library-owned copy stream while the first
+ * degree step runs panel by panel on the handle's stream; steps 2..degree start once
+ * the whole of H is resident. d_Y must already hold Y. Pinned h_H overlaps the upload
+ * with the first step; pageable h_H is staged panel by panel. Returns once h_H has
+ * been read (the filter may still run on the stream); d_H then holds H. */
+int chfsi_filter_streamed(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a,
+                          double b, double lam_ref, const void* h_H, int64_t ldh_host, void* d_H,
+                          int64_t ldh, void* d_Y, int64_t ldy, void* d_W, int64_t ldw, int panels,
+                          int* h_result_in_w);
+
 /* One fused degree step C = alpha H Y1 + beta Y1 + gamma Y0 (Y0 may be NULL and may
  * alias C); the unit the filter roofline is measured on (core.py:280-281). */
 int chfsi_filter_step(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,

@@ -267,6 +267,9 @@ def chebyshev_filter(H, Y, spec):
             f"lam_ref = {spec.lam_ref} lies inside the unwanted interval [{spec.a}, {spec.b}]; "
             f"wanted and unwanted intervals overlap (a larger buffer improves the "
             f"lambda_nev+1 estimate)")
+    host_h = _streamable_host(H)
+    if host_h is not None:
+        return _filter_streamed(host_h, Y, spec)
     hm = _hermitian(H)
     if isinstance(Y, VectorBlock):
         yb = Y.device_block(hm.device_block().device).clone()
@@ -282,6 +285,48 @@ def chebyshev_filter(H, Y, spec):
     w = torch.empty_like(yb)
     out = engine(yb.device).filter(hm.device_block(), yb, w, spec.degree, spec.a, spec.b,
                                    spec.lam_ref)
+    _count_products(spec.degree * dev.cols(yb))
+    return VectorBlock(out)
+
+
+# Host operators at least this large are uploaded panel by panel under the first
+# degree step (chfsi_filter_streamed) instead of before the filter.
+_STREAM_MIN_N = 4096
+
+
+def _streamable_host(H):
+    """F-order complex128 host copy of a raw (reference-style ndarray) operator large
+    enough to stream, else None. Wrapped operators are already resident."""
+    if isinstance(H, (HermitianDenseMatrix, VectorBlock, LowerTriangularFactor, torch.Tensor)):
+        return None
+    if hasattr(H, "entries"):
+        return None
+    a = np.asarray(H)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < _STREAM_MIN_N:
+        return None
+    return np.asfortranarray(a, dtype=np.complex128)
+
+
+def _filter_streamed(host_h, Y, spec):
+    """chebyshev_filter for a host ndarray H: the upload of H overlaps the first degree
+    step (core.py:304 uses the raw array as is; so does this -- no Hermitian check)."""
+    n = host_h.shape[0]
+    device = default_device()
+    if isinstance(Y, VectorBlock):
+        yb = Y.device_block(device).clone()
+    else:
+        y = _host_block(Y)
+        y2d = y if y.ndim == 2 else y.reshape(-1, 1)
+        if y2d.shape[0] != n:
+            raise ContractViolation(
+                f"filter operand mismatch: H is {(n, n)}, Y has {y2d.shape[0]} rows")
+        yb = dev.to_device(y2d, device)
+    if dev.rows(yb) != n:
+        raise ContractViolation(f"filter operand mismatch: H is {(n, n)}, Y has {dev.rows(yb)} rows")
+    hdev = dev.empty(n, n, device)
+    w = torch.empty_like(yb)
+    out = engine(device).filter_streamed(host_h, hdev, yb, w, spec.degree, spec.a, spec.b,
+                                         spec.lam_ref)
     _count_products(spec.degree * dev.cols(yb))
     return VectorBlock(out)
 

@@ -59,6 +59,10 @@ int heevd(Handle* h, long long n, double2* A, long long lda, double* w_dev);
 int filter(Handle* h, long long n, long long k, int degree, double a, double b, double lam_ref,
            const double2* H, long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
            int* result_in_w);
+int filter_streamed(Handle* h, long long n, long long k, int degree, double a, double b,
+                    double lam_ref, const double2* H_host, long long ldh_host, double2* H,
+                    long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
+                    int panels, int* result_in_w);
 int lanczos_bound(Handle* h, long long n, int k, const double2* H, long long ldh,
                   const double2* v0, double* alphas, double* betas, int* steps, double* bound);
 int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ldf,
@@ -198,6 +202,7 @@ int chfsi_destroy(chfsi_handle_t h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
   destroy_filter_graphs(h);
+  destroy_copy_stream(h);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   for (int i = 0; i < Handle::kSlots; ++i)
     if (h->scratch[i]) cudaFree(h->scratch[i]);
@@ -250,6 +255,24 @@ int chfsi_filter(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a, d
   }
   return filter(h, n, k, degree, a, b, lam_ref, (const double2*)d_H, ldh, (double2*)d_Y, ldy,
                 (double2*)d_W, ldw, h_result_in_w);
+}
+
+int chfsi_filter_streamed(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a,
+                          double b, double lam_ref, const void* h_H, int64_t ldh_host, void* d_H,
+                          int64_t ldh, void* d_Y, int64_t ldy, void* d_W, int64_t ldw, int panels,
+                          int* h_result_in_w) {
+  H_CHECK(h);
+  if (!(a < b)) {
+    set_error("filter interval requires a < b");
+    return ERR_ARG;
+  }
+  if (!h_H || !d_H) {
+    set_error("filter_streamed: null H");
+    return ERR_ARG;
+  }
+  return filter_streamed(h, n, k, degree, a, b, lam_ref, (const double2*)h_H, ldh_host,
+                         (double2*)d_H, ldh, (double2*)d_Y, ldy, (double2*)d_W, ldw, panels,
+                         h_result_in_w);
 }
 
 int chfsi_filter_step(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,

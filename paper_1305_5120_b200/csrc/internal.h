@@ -59,9 +59,13 @@ struct Handle {
   cudaStream_t capture_stream = nullptr;  // private: the legacy default stream cannot capture
   double2* ws_override = nullptr;
   size_t ws_override_bytes = 0;
+  // host->device upload stream and its per-panel events (streamed filter)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t>* copy_events = nullptr;
 };
 
 void destroy_filter_graphs(Handle* h);
+void destroy_copy_stream(Handle* h);
 
 // scratch slots
 enum Slot : int {
@@ -115,6 +119,12 @@ int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, lon
                       const double2* Y1, long long ld1, double alpha, double beta,
                       const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
                       const double* coef_dev = nullptr);
+// Row panel of a fused step: rows [r0, r0 + M) of C = alpha*A*B + beta*Y1e + gamma*Y0
+// with A = H + r0 (M x K), B the full K x N block and Y1e = B + r0.
+int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const double2* A,
+                       long long lda, const double2* B, long long ldb, const double2* Y1e,
+                       long long ld1e, double alpha, double beta, const double2* Y0, long long ld0,
+                       double gamma, double2* C, long long ldc, const double* coef_dev);
 // split-K workspace bytes the filter step's plan needs (pre-sized before graph capture)
 size_t filter_step_workspace(Handle* h, long long M, long long N);
 

@@ -78,6 +78,45 @@ int heevd(Handle* h, long long n, double2* A, long long lda, double* w_dev) {
   return OK;
 }
 
+// Scaled three-term recurrence coefficients {alpha, beta, gamma} per degree step
+// (core.py:263-284 `_filter_raw`).
+static std::vector<double> filter_coefs(int degree, double a, double b, double lam_ref) {
+  std::vector<double> coef(3 * (size_t)degree);
+  const double c = (a + b) / 2.0;
+  const double e = (b - a) / 2.0;
+  const double sigma1 = e / (lam_ref - c);
+  double sigma = sigma1;
+  // y1 = sigma1/e * H y - c*sigma1/e * y
+  coef[0] = sigma1 / e;
+  coef[1] = -c * sigma1 / e;
+  coef[2] = 0.0;
+  for (int j = 1; j < degree; ++j) {
+    // y2 = scale*(H y1) - c*scale*y1 - sigma*sigma_new*y0, written over y0
+    const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+    const double scale = 2.0 * sigma_new / e;
+    coef[3 * j] = scale;
+    coef[3 * j + 1] = -c * scale;
+    coef[3 * j + 2] = -(sigma * sigma_new);
+    sigma = sigma_new;
+  }
+  return coef;
+}
+
+// Degree steps j0 .. degree-1 (step j0 - 1 left its result in `cur`, its input in `prev`).
+static int filter_steps(Handle* h, long long n, long long k, int degree, int j0, const double* coef,
+                        const double* coef_dev, const double2* H, long long ldh, double2* prev,
+                        long long ldp, double2* cur, long long ldc, double2* W,
+                        int* result_in_w) {
+  for (int j = j0; j < degree; ++j) {
+    CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, coef[3 * j], coef[3 * j + 1], prev, ldp,
+                                coef[3 * j + 2], prev, ldp, coef_dev ? coef_dev + 3 * j : nullptr));
+    std::swap(prev, cur);
+    std::swap(ldp, ldc);
+  }
+  *result_in_w = (cur == W) ? 1 : 0;
+  return OK;
+}
+
 int filter(Handle* h, long long n, long long k, int degree, double a, double b, double lam_ref,
            const double2* H, long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
            int* result_in_w) {
@@ -85,27 +124,7 @@ int filter(Handle* h, long long n, long long k, int degree, double a, double b, 
     set_error("filter degree must be >= 1");
     return ERR_ARG;
   }
-  // scaled three-term recurrence coefficients {alpha, beta, gamma} per degree step
-  std::vector<double> coef(3 * (size_t)degree);
-  {
-    const double c = (a + b) / 2.0;
-    const double e = (b - a) / 2.0;
-    const double sigma1 = e / (lam_ref - c);
-    double sigma = sigma1;
-    // y1 = sigma1/e * H y - c*sigma1/e * y
-    coef[0] = sigma1 / e;
-    coef[1] = -c * sigma1 / e;
-    coef[2] = 0.0;
-    for (int j = 1; j < degree; ++j) {
-      // y2 = scale*(H y1) - c*scale*y1 - sigma*sigma_new*y0, written over y0
-      const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
-      const double scale = 2.0 * sigma_new / e;
-      coef[3 * j] = scale;
-      coef[3 * j + 1] = -c * scale;
-      coef[3 * j + 2] = -(sigma * sigma_new);
-      sigma = sigma_new;
-    }
-  }
+  const std::vector<double> coef = filter_coefs(degree, a, b, lam_ref);
   if (filter_graphs_enabled())
     return filter_graphed(h, n, k, degree, coef.data(), H, ldh, Y, ldy, W, ldw, result_in_w);
   return filter_issue(h, n, k, degree, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, result_in_w);
@@ -118,18 +137,81 @@ static int filter_issue(Handle* h, long long n, long long k, int degree, const d
                         long long ldy, double2* W, long long ldw, int* result_in_w) {
   CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, Y, ldy, coef[0], coef[1], nullptr, 0, 0.0, W, ldw,
                               coef_dev));
-  double2* prev = Y;
-  long long ldp = ldy;
-  double2* cur = W;
-  long long ldc = ldw;
-  for (int j = 1; j < degree; ++j) {
-    CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, coef[3 * j], coef[3 * j + 1], prev, ldp,
-                                coef[3 * j + 2], prev, ldp, coef_dev ? coef_dev + 3 * j : nullptr));
-    std::swap(prev, cur);
-    std::swap(ldp, ldc);
+  return filter_steps(h, n, k, degree, 1, coef, coef_dev, H, ldh, Y, ldy, W, ldw, W, result_in_w);
+}
+
+// Filter whose operator arrives from host memory (core.py:287-311 `chebyshev_filter`
+// called with an ndarray H): H is uploaded in `panels` row panels on a copy stream
+// (strided 2-D copies of the column-major rows [r0, r1)), and the first degree step
+// runs panel by panel as the rows land -- output rows [r0, r1) need only H[r0:r1, :]
+// and the (already resident) Y. Degree steps 2.. need all of H and start once the last
+// panel is in. With pinned host memory the upload (PCIe) hides behind the first step
+// except for one panel. Every panel step accumulates each output over K in the same
+// order as the full-height step, so the result is identical when no panel uses split-K.
+int filter_streamed(Handle* h, long long n, long long k, int degree, double a, double b,
+                    double lam_ref, const double2* H_host, long long ldh_host, double2* H,
+                    long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
+                    int panels, int* result_in_w) {
+  if (degree < 1) {
+    set_error("filter degree must be >= 1");
+    return ERR_ARG;
   }
-  *result_in_w = (cur == W) ? 1 : 0;
+  if (n <= 0 || k <= 0) {
+    *result_in_w = 0;
+    return OK;
+  }
+  if (ldh_host < n || ldh < n) {
+    set_error("filter_streamed: leading dimensions must be >= n");
+    return ERR_ARG;
+  }
+  if (panels <= 0) panels = n >= 8192 ? 8 : (n >= 2048 ? 4 : 1);
+  // panel height: a multiple of 64 rows (the CTA tile height)
+  long long rows = (n + panels - 1) / panels;
+  rows = ((rows + 63) / 64) * 64;
+  panels = (int)((n + rows - 1) / rows);
+  if (!h->copy_stream)
+    CHFSI_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  if (!h->copy_events) h->copy_events = new std::vector<cudaEvent_t>();
+  auto& ev = *h->copy_events;
+  while ((int)ev.size() < panels + 1) {
+    cudaEvent_t e;
+    CHFSI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev.push_back(e);
+  }
+  const std::vector<double> coef = filter_coefs(degree, a, b, lam_ref);
+  // the destination may still be read by earlier work queued on the compute stream
+  CHFSI_CUDA(cudaEventRecord(ev[panels], h->stream));
+  CHFSI_CUDA(cudaStreamWaitEvent(h->copy_stream, ev[panels], 0));
+  for (int p = 0; p < panels; ++p) {
+    const long long r0 = p * rows;
+    const long long m = std::min(rows, n - r0);
+    CHFSI_CUDA(cudaMemcpy2DAsync(H + r0, (size_t)ldh * sizeof(double2), H_host + r0,
+                                 (size_t)ldh_host * sizeof(double2), (size_t)m * sizeof(double2),
+                                 (size_t)n, cudaMemcpyHostToDevice, h->copy_stream));
+    CHFSI_CUDA(cudaEventRecord(ev[p], h->copy_stream));
+    // enqueue the panel's step right behind its copy: with pageable host memory the
+    // copy call returns only once staged, and the step of panel p then overlaps the
+    // staging of panel p + 1
+    CHFSI_CUDA(cudaStreamWaitEvent(h->stream, ev[p], 0));
+    CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0], coef[1],
+                                 nullptr, 0, 0.0, W + r0, ldw, nullptr));
+  }
+  CHFSI_TRY(filter_steps(h, n, k, degree, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, W,
+                         result_in_w));
+  // everything is queued; return once the host buffer has been read so the caller
+  // may free or reuse it (the GPU keeps filtering meanwhile)
+  CHFSI_CUDA(cudaEventSynchronize(ev[panels - 1]));
   return OK;
+}
+
+void destroy_copy_stream(Handle* h) {
+  if (h->copy_events) {
+    for (cudaEvent_t e : *h->copy_events) cudaEventDestroy(e);
+    delete h->copy_events;
+    h->copy_events = nullptr;
+  }
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  h->copy_stream = nullptr;
 }
 
 // Opt-in (CHFSI_FILTER_GRAPHS=1). Measured on B200 (scripts/graph_micro.py): a replay

@@ -373,7 +373,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   const int threads = 256;
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);
   zgemm_splitk_reduce_kernel<<<blocks, threads, 0, h->stream>>>(
-      (int)M, (int)N, pl.split, ws, epi, p.alpha, p.beta, p.C, p.ldc, p.B, p.ldb, p.Y0, p.ld0,
+      (int)M, (int)N, pl.split, ws, epi, p.alpha, p.beta, p.C, p.ldc, p.Y1e, p.ld1e, p.Y0, p.ld0,
       p.gamma, epi == EPI_FILTER ? p.coef : nullptr);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
@@ -422,19 +422,28 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
   return launch(h, opa, opb, EPI_STORE, M, N, K, p);
 }
 
-int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
-                      const double2* Y1, long long ld1, double alpha, double beta,
-                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
-                      const double* coef_dev) {
+int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const double2* A,
+                       long long lda, const double2* B, long long ldb, const double2* Y1e,
+                       long long ld1e, double alpha, double beta, const double2* Y0, long long ld0,
+                       double gamma, double2* C, long long ldc, const double* coef_dev) {
   GemmParams p{};
   p.A = A; p.lda = lda;
-  p.B = Y1; p.ldb = ld1;
+  p.B = B; p.ldb = ldb;
   p.C = C; p.ldc = ldc;
   p.alpha = make_double2(alpha, 0.0);
   p.beta = make_double2(beta, 0.0);
   p.Y0 = Y0; p.ld0 = ld0; p.gamma = gamma;
+  p.Y1e = Y1e; p.ld1e = ld1e;
   p.coef = coef_dev;
-  return launch(h, OP_N, OP_N, EPI_FILTER, M, N, M, p);
+  return launch(h, OP_N, OP_N, EPI_FILTER, M, N, K, p);
+}
+
+int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
+                      const double2* Y1, long long ld1, double alpha, double beta,
+                      const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
+                      const double* coef_dev) {
+  return zgemm_filter_panel(h, M, N, M, A, lda, Y1, ld1, Y1, ld1, alpha, beta, Y0, ld0, gamma, C,
+                            ldc, coef_dev);
 }
 
 size_t filter_step_workspace(Handle* h, long long M, long long N) {

@@ -32,8 +32,10 @@ struct GemmParams {
   const double2* B; long long ldb;
   double2* C; long long ldc;
   double2 alpha, beta;
-  // EPI_FILTER: Y0 (may alias C) and its real coefficient gamma
+  // EPI_FILTER: Y0 (may alias C) and its real coefficient gamma; Y1e is the beta
+  // operand (rows aligned with C): B itself for a full step, B + r0 for a row panel
   const double2* Y0; long long ld0; double gamma;
+  const double2* Y1e; long long ld1e;
   // EPI_PARTIAL: K range per blockIdx.z and the [z][N][M] workspace
   int k_chunk;
   double2* ws;
@@ -215,7 +217,7 @@ zgemm_dmma_kernel(const GemmParams p) {
           // out = alpha*acc + beta*Y1 + gamma*Y0 with real coefficients
           double fa, fb, fg;
           filter_coef(p, fa, fb, fg);
-          const double2 y1 = p.B[m + (long long)n * p.ldb];
+          const double2 y1 = p.Y1e[m + (long long)n * p.ld1e];
           double orr = fa * xr + fb * y1.x;
           double oi = fa * xi + fb * y1.y;
           if (p.Y0 != nullptr) {

@@ -289,7 +289,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
         } else if (EPI == EPI_FILTER) {
           double fa, fb, fg;
           filter_coef(p, fa, fb, fg);
-          const double2 y1 = p.B[m + (long long)n * p.ldb];
+          const double2 y1 = p.Y1e[m + (long long)n * p.ld1e];
           double orr = fa * xr + fb * y1.x;
           double oi = fa * xi + fb * y1.y;
           if (p.Y0 != nullptr) {

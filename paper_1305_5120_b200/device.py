@@ -148,6 +148,23 @@ class Engine:
                      ctypes.byref(flag))
         return W if flag.value else Y
 
+    def filter_streamed(self, host_H, H, Y, W, degree, a, b, lam_ref, panels=0):
+        """p_m(H) Y with H uploaded from the host F-order array ``host_H`` into the
+        device block ``H`` while the first degree step runs panel by panel
+        (chfsi_filter_streamed; it returns once host_H has been read, the GPU still busy);
+        Y is clobbered. Returns the tensor holding the result (Y or W)."""
+        if not (isinstance(host_H, np.ndarray) and host_H.dtype == np.complex128
+                and host_H.flags.f_contiguous and host_H.ndim == 2):
+            raise ValueError("filter_streamed: host_H must be an F-contiguous complex128 matrix")
+        n, k = rows(Y), cols(Y)
+        if host_H.shape != (n, n) or rows(H) != n or cols(H) != n:
+            raise ValueError("filter_streamed: H must be n x n with n = rows(Y)")
+        flag = ctypes.c_int(0)
+        _native.call("chfsi_filter_streamed", self.h, n, k, int(degree), float(a), float(b),
+                     float(lam_ref), host_H.ctypes.data, n, ptr(H), ld(H), ptr(Y), ld(Y),
+                     ptr(W), ld(W), int(panels), ctypes.byref(flag))
+        return W if flag.value else Y
+
     def filter_step(self, H, Y1, alpha, beta, Y0, gamma, C):
         n, k = rows(Y1), cols(Y1)
         _native.call("chfsi_filter_step", self.h, n, k, ptr(H), ld(H), ptr(Y1), ld(Y1),

@@ -92,6 +92,75 @@ def test_filter_matches_oracle_recurrence(eng, n, k, m):
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("n,k,m,panels", [(513, 37, 7, 3), (1000, 120, 12, 0), (1000, 120, 5, 16),
+                                          (200, 1, 3, 1)])
+def test_filter_streamed_matches_oracle(eng, n, k, m, panels):
+    """Host-H filter (upload overlapped with the first degree step, row panels, ragged
+    last panel) against the oracle recurrence; H lands on the device unchanged."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    h, lam, _ = baseline_matrix(n, n)
+    h = np.asfortranarray(h)
+    rng = np.random.default_rng(n + 3 * k)
+    y = crand(rng, n, k)
+    a, b, lam_ref = float(lam[min(k, n - 1)]), float(lam[-1]) * 1.05, float(lam[0])
+    ref = O.cheb_filter(h, y, m, a, b, lam_ref)
+    dH = D.empty(n, n, eng.device)
+    dY = D.to_device(y, eng.device)
+    dW = D.zeros(n, k, eng.device)
+    got = D.to_host(eng.filter_streamed(h, dH, dY, dW, m, a, b, lam_ref, panels=panels))
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.array_equal(D.to_host(dH), h)
+
+
+def test_filter_streamed_bit_identical_without_split(eng):
+    """With split-K off, every panel step sums each output over K in the order of the
+    full-height step: the streamed filter equals the resident one bit for bit."""
+    from paper_1305_5120_b200 import _native
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    n, k, m = 1536, 96, 6
+    h, lam, _ = baseline_matrix(n, n)
+    h = np.asfortranarray(h)
+    y = crand(np.random.default_rng(5), n, k)
+    a, b, lam_ref = float(lam[k]), float(lam[-1]) * 1.05, float(lam[0])
+    lib = _native.load()
+    assert lib.chfsi_gemm_override(-1, 1) == 0
+    try:
+        dH = D.to_device(h, eng.device)
+        full = D.to_host(eng.filter(dH, D.to_device(y, eng.device), D.zeros(n, k, eng.device),
+                                    m, a, b, lam_ref))
+        dH2 = D.empty(n, n, eng.device)
+        got = D.to_host(eng.filter_streamed(h, dH2, D.to_device(y, eng.device),
+                                            D.zeros(n, k, eng.device), m, a, b, lam_ref, panels=4))
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+    assert np.array_equal(got, full)
+
+
+def test_chebyshev_filter_host_path_streams(eng, monkeypatch):
+    """The public chebyshev_filter(ndarray H, ...) takes the streamed path above the size
+    threshold and returns the same block as with H already wrapped on the device."""
+    import paper_1305_5120_b200 as G
+    import paper_1305_5120_b200.core as C
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    n, k = 700, 40
+    h, lam, _ = baseline_matrix(n, n)
+    y = crand(np.random.default_rng(8), n, k)
+    spec = G.FilterSpec(degree=9, a=float(lam[k]), b=float(lam[-1]) * 1.05, lam_ref=float(lam[0]))
+    monkeypatch.setattr(C, "_STREAM_MIN_N", 512)
+    calls = []
+    orig = C._filter_streamed
+    monkeypatch.setattr(C, "_filter_streamed", lambda *a: calls.append(1) or orig(*a))
+    got = G.chebyshev_filter(h, y, spec).entries
+    assert calls == [1]
+    ref = G.chebyshev_filter(G.HermitianDenseMatrix(h), y, spec).entries
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    with pytest.raises(G.ContractViolation):
+        G.chebyshev_filter(h, y[:-1], spec)
+
+
 def test_lanczos_bound_matches_oracle(eng):
     import oracle.chfsi_oracle as O
     import paper_1305_5120_b200 as G
