@@ -11,7 +11,7 @@ import os
 from .errors import ChfsiError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libchfsi_b200.so")
+LIB_PATH = os.environ.get("CHFSI_LIB") or os.path.join(_HERE, "_lib", "libchfsi_b200.so")
 
 # status codes (include/chfsi_b200.h)
 ERR_ARG = -1

@@ -8,6 +8,7 @@
 // are bit-identical run to run (reference criterion 7, test_acceptance.py:199).
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cmath>
 #include <string>
 #include <unordered_map>
@@ -84,7 +85,7 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 10;
+constexpr int NCFG = 11;
 constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
 // cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
 // cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
@@ -98,6 +99,8 @@ using C4 = CfgT<64, 64, 16, 32, 32, 3>;
 using C5 = CfgT<128, 64, 8, 32, 32, 4>;
 using C6 = CfgT<128, 32, 8, 32, 16, 4>;
 // cfg 7: TMA 64x32 warp 32x16, 4 stages; cfg 8: TMA 64x16 warp 16x16; cfg 9: TMA 64x64 warp 32x32
+// cfg 10: TMA 64x32 with four 16x32 warps stacked by rows (same fragment loads per DMMA as
+// cfg 7; on a ragged column edge every warp keeps the same number of live 8-column blocks)
 using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmParams);
 template <int BM, int BN, int WM, int WN, int ST, int MINB = 1>
 struct TmaT {
@@ -111,12 +114,11 @@ struct TmaT {
 using T7 = TmaT<64, 32, 32, 16, 4, 4>;
 using T8 = TmaT<64, 16, 16, 16, 4, 4>;
 using T9 = TmaT<64, 64, 32, 32, 4, 2>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8};
-// relative per-tile throughput (measured on B200, see profiles/); bigger warp tiles
-// amortise fragment loads and barriers
-double g_eff[NCFG] = {0.98, 1.00, 0.96, 0.90, 0.96, 0.90, 0.975, 1.045, 0.99, 0.93};
+using T10 = TmaT<64, 32, 16, 32, 4, 4>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8};
+const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32};  // warp tile width
 bool g_tma_enabled = true;
 int g_force_cfg = -1, g_force_split = 0;
 
@@ -170,6 +172,7 @@ int ensure_table() {
   put_tma<T7>(7);
   put_tma<T8>(8);
   put_tma<T9>(9);
+  put_tma<T10>(10);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -185,6 +188,12 @@ int ensure_table() {
           en.ready = true;
         }
   g_table_init = true;
+  if (getenv("CHFSI_PLAN_DEBUG")) {
+    for (int c = 0; c < NCFG; ++c)
+      fprintf(stderr, "chfsi cfg %d: occ NN store %d filter %d partial %d, CN store %d partial %d\n", c,
+              g_table[c][0][0][0].occ, g_table[c][0][0][1].occ, g_table[c][0][0][2].occ,
+              g_table[c][1][0][0].occ, g_table[c][1][0][2].occ);
+  }
   return OK;
 }
 
@@ -194,11 +203,62 @@ struct Plan {
   int k_chunk = 0;
 };
 
-// Estimated cost ~ waves * resident CTAs * padded tile work; smaller is better.
+// Launch-time model (microseconds), fitted by scripts/fit_cost_model.py to 2900
+// measured (shape, config, split) points on B200 (profiles/r01/tune_sweep_*.json; the
+// model's pick is within 1.8 % of the best measured plan on geometric mean):
+//   * every SM runs q = ceil(CTAs / SMs) CTAs, at most occ at a time; r CTAs sharing
+//     the SM's DMMA pipe progress at min(1, r / R0) of it, so a round of r costs
+//     W * max(r, R0) / (eff * peak), W = BM * live columns * K-chunk;
+//   * a ragged last column tile does DMMA work for its live 8-column blocks only but
+//     costs at least kFloor of a full tile (its loads are not skipped); when its live
+//     blocks are spread unevenly over the warp columns the CTA waits for the heavy
+//     warps (ncu: DMMA pipe 92.5 % vs 95.7 % active at k = 210): x (1 + kRag / tiles_n);
+//   * split-K adds the reduce pass: kTred + (s + 3) M N 16 B at HBM speed.
+constexpr double kEffNN[NCFG] = {0.906, 0.898, 0.837, 0.823, 0.911, 0.926, 0.885,
+                                 0.966, 0.915, 0.962, 0.954};
+constexpr double kEffCN[7] = {0.886, 0.927, 0.877, 0.854, 1.058, 0.971, 0.887};
+constexpr double kR0Warps4 = 1.289, kR0Warps8 = 1.108;
+constexpr double kRag = 0.122, kFloor = 0.859;
+constexpr double kT0 = 5.583, kTred = 3.101, kHbmBytesPerUs = 6.58e6;
+constexpr double kPeakCmacPerUsPerSm = 37.16e12 / 8.0 / 1e6 / 148.0;
+
+double plan_cost(int c, int occ, int threads, bool nn, int sms, long long M, long long N,
+                 long long K, int s) {
+  const long long tm = (M + kBM[c] - 1) / kBM[c];
+  const long long tn = (N + kBN[c] - 1) / kBN[c];
+  const long long ctas = tm * tn * s;
+  const long long q = (ctas + sms - 1) / sms;
+  const double r0 = threads >= 256 ? kR0Warps8 : kR0Warps4;
+  const double kchunk = (double)((K + s - 1) / s);
+  const long long last = ((N - (tn - 1) * kBN[c] + 7) / 8) * 8;
+  const double live = ((double)(tn - 1) * kBN[c] +
+                       std::max((double)last, kFloor * kBN[c])) / (double)tn;
+  const double W = kBM[c] * live * kchunk;
+  const long long full = q / occ, rem = q % occ;
+  const double rounds = (double)full * std::max((double)occ, r0) +
+                        (rem ? std::max((double)rem, r0) : 0.0);
+  const double eff = nn ? kEffNN[c] : kEffCN[std::min(c, 6)];
+  double t = W * rounds / (eff * kPeakCmacPerUsPerSm);
+  // live 8-column blocks of the last column tile per warp column
+  const int per = kWN[c] / 8, wcols = kBN[c] / kWN[c];
+  const int vb = (int)(last / 8);
+  int lo = per, hi = 0;
+  for (int w = 0; w < wcols; ++w) {
+    const int l = std::max(0, std::min(per, vb - w * per));
+    lo = std::min(lo, l);
+    hi = std::max(hi, l);
+  }
+  if (hi != lo) t *= 1.0 + kRag / (double)tn;
+  t += kT0;
+  if (s > 1) t += kTred + (double)(s + 3) * (double)M * (double)N * 16.0 / kHbmBytesPerUs;
+  return t;
+}
+
 Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
   Plan best;
   double best_cost = 1e300;
   const int sms = h->sm_count;
+  const bool nn = (opa == OP_N && opb == OP_N);
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
     if (c >= FIRST_TMA && !g_tma_enabled) continue;
@@ -206,26 +266,18 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
     if (!e.ready && !ep.ready) continue;
     const int bk = kBKc[c];
-    const long long tm = (M + kBM[c] - 1) / kBM[c];
-    const long long tn = (N + kBN[c] - 1) / kBN[c];
-    const long long tiles = tm * tn;
     const long long ktiles = std::max<long long>(1, (K + bk - 1) / bk);
     int max_split = (int)std::min<long long>(64, ktiles / (32 / bk));
-    if (M * N * 16LL * 8 > (2LL << 30)) max_split = 1;  // cap workspace
+    // cap the split-K workspace at 1 GiB
+    const long long ws_cap = (1LL << 30) / std::max<long long>(1, M * N * 16LL);
+    max_split = (int)std::min<long long>(max_split, std::max<long long>(1, ws_cap));
     int s_lo = 1, s_hi = std::max(1, max_split);
     if (g_force_split > 0) s_lo = s_hi = g_force_split;
     for (int s = s_lo; s <= s_hi; ++s) {
       const Entry& en = (s == 1) ? e : ep;
       if (!en.ready) continue;
       const long long kt_per = (ktiles + s - 1) / s;
-      const long long ctas = tiles * s;
-      const long long slots = (long long)en.occ * sms;
-      const long long waves = (ctas + slots - 1) / slots;
-      const long long resident = std::min<long long>(en.occ, (ctas + sms - 1) / sms);
-      // per-wave time ~ resident CTAs sharing one SM x padded tile work / tile efficiency
-      double cost = (double)waves * (double)resident *
-                    ((double)kBM[c] * kBN[c] * (kt_per * bk + 64.0)) / g_eff[c];
-      if (s > 1) cost += (double)M * N * s * 0.5;  // reduce traffic
+      const double cost = plan_cost(c, en.occ, en.threads, nn, sms, M, N, K, s);
       if (cost < best_cost * 0.999) {
         best_cost = cost;
         best.cfg = c;

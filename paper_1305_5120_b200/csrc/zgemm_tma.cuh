@@ -76,6 +76,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 __device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); }
 
+// Stage refill lag: at k-tile kt the producer lane refills the stage of tile
+// kt - kDefer (released by every warp kDefer iterations earlier).
+#ifndef CHFSI_TMA_DEFER
+#define CHFSI_TMA_DEFER 1
+#endif
+constexpr int kDefer = CHFSI_TMA_DEFER;
+
 template <int BM, int BN, int WM, int WN, int STAGES>
 constexpr int zgemm_tma_smem_bytes() {
   return STAGES * (BM * 8 + BN * 8) * 16 + 1024 /* alignment slack */ + 2 * STAGES * 8;
@@ -209,9 +216,9 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       // every warp has normally finished tile kt - 1, so this empty-barrier wait is
       // almost always already complete and the producer lane does not stall its warp
       // (waiting on the just-released stage cost ~8 % of warp samples, profiles/r01)
-      if (lane == 0 && kt >= 1 && warp == (kt % NWARP) && kt - 1 + STAGES < KT) {
-        mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        issue(kt - 1 + STAGES);
+      if (lane == 0 && kt >= kDefer && warp == (kt % NWARP) && kt - kDefer + STAGES < KT) {
+        mbar_wait(&empty[(kt - kDefer) % STAGES], ((kt - kDefer) / STAGES) & 1);
+        issue(kt - kDefer + STAGES);
       }
     }
   } else {  // ragged column edge: skip 8-column blocks past N
@@ -265,9 +272,9 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       // every warp has normally finished tile kt - 1, so this empty-barrier wait is
       // almost always already complete and the producer lane does not stall its warp
       // (waiting on the just-released stage cost ~8 % of warp samples, profiles/r01)
-      if (lane == 0 && kt >= 1 && warp == (kt % NWARP) && kt - 1 + STAGES < KT) {
-        mbar_wait(&empty[(kt - 1) % STAGES], ((kt - 1) / STAGES) & 1);
-        issue(kt - 1 + STAGES);
+      if (lane == 0 && kt >= kDefer && warp == (kt % NWARP) && kt - kDefer + STAGES < KT) {
+        mbar_wait(&empty[(kt - kDefer) % STAGES], ((kt - kDefer) / STAGES) & 1);
+        issue(kt - kDefer + STAGES);
       }
     }
   }

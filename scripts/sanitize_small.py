@@ -19,7 +19,7 @@ def crand(*s):
     return rng.standard_normal(s) + 1j * rng.standard_normal(s)
 
 
-for cfg in range(10):
+for cfg in range(11):
     for split in (1, 2):
         lib.chfsi_gemm_override(cfg, split)
         for (m, n, k) in [(13, 5, 27), (70, 33, 9)]:

@@ -31,7 +31,7 @@ for k in widths:
     lib.chfsi_gemm_plan(eng.h, 0, 0, 1, n, k, n, ctypes.byref(cfg), ctypes.byref(spl))
     row = {"plan": [cfg.value, spl.value]}
     reps = max(1, min(10, int(3e12 / (8.0 * n * n * k))))
-    for c in range(10):
+    for c in range(11):
         for s in ((1, 2, 3, 4) if k <= 300 else (1,)):
             lib.chfsi_gemm_override(c, s)
             eng.filter_step(H, Y1, 0.5, -0.1, Y0, 0.2, Y0)

@@ -290,7 +290,7 @@ def test_cholesky_trtri_heevd(eng):
 
 
 # every tile configuration and split factor the cost model can pick, on ragged shapes
-_NCFG = 10
+_NCFG = 11
 _TMA_FIRST = 7
 
 
