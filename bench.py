@@ -350,6 +350,7 @@ KERNELS = {
     7: "zgemm_tma_kernel<64,32,warp32x16,TMA+mbarrier x4,EPI_FILTER>",
     8: "zgemm_tma_kernel<64,16,warp16x16,TMA+mbarrier x4,EPI_FILTER>",
     9: "zgemm_tma_kernel<64,64,warp32x32,TMA+mbarrier x4,EPI_FILTER>",
+    10: "zgemm_tma_kernel<64,32,warp16x32,TMA+mbarrier x4,EPI_FILTER>",
 }
 
 
@@ -392,7 +393,8 @@ def c4_iteration_window(n=20000, nev=2000, nex=200, degree=25):
 def generalized_c4_setup(n=20000):
     """Per-problem generalized-to-standard cost at c4 scale (core.py:549-569): S = I +
     0.1 B^H B / ||B^H B|| (norm from a 10-step Lanczos bound), zpotrf, blocked
-    triangular inverse, H = L^-1 A L^-H (two DMMA GEMMs), Hermitian check/symmetrise."""
+    triangular inverse, H = L^-1 A L^-H (two DMMA GEMMs skipping the zero triangle of
+    L^-1), Hermitian check/symmetrise."""
     import torch
     from paper_1305_5120_b200 import device as D
     from paper_1305_5120_b200 import workloads as Wl
@@ -424,11 +426,14 @@ def generalized_c4_setup(n=20000):
     t["trtri_s"] = time.perf_counter() - t0
     w = torch.empty_like(s)
     t0 = time.perf_counter()
-    eng.zgemm("N", "N", n, n, n, 1.0, linv, a, 0.0, w)
-    eng.zgemm("N", "C", n, n, n, 1.0, w, linv, 0.0, a)
+    h = torch.empty_like(s)
+    eng.reduce_to_standard(a, linv, w, h)  # two GEMMs skipping L^-1's zero triangle
     torch.cuda.synchronize()
     t["reduce_gemms_s"] = time.perf_counter() - t0
-    t["reduce_gemms_tflops"] = 2 * 8.0 * n ** 3 / t["reduce_gemms_s"] / 1e12
+    # algorithmic work 8 n^3 flop: each GEMM multiplies by a triangular factor (4 n^3)
+    t["reduce_gemms_tflops"] = 8.0 * n ** 3 / t["reduce_gemms_s"] / 1e12
+    t["reduce_dense_equivalent_tflops"] = 16.0 * n ** 3 / t["reduce_gemms_s"] / 1e12
+    a = h
     t0 = time.perf_counter()
     fro, devn = eng.hermitian_norms(a)
     eng.hermitize(a)

@@ -136,6 +136,14 @@ int chfsi_cholesky(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, int* h_i
 int chfsi_trtri_lower(chfsi_handle_t h, int64_t n, const void* d_L, int64_t ldl, void* d_X,
                       int64_t ldx);
 
+/* core.py:172-188 `reduce_to_standard`: H = L^-1 A L^-H given d_Linv = L^-1 (lower
+ * triangular with a zero upper triangle, e.g. from chfsi_trtri_lower). Two DMMA GEMMs
+ * that skip the zero triangle of Linv; d_W is an n x n work block. H is not
+ * re-symmetrised here (chfsi_hermitian_norms / chfsi_hermitize do that). */
+int chfsi_reduce_to_standard(chfsi_handle_t h, int64_t n, const void* d_A, int64_t lda,
+                             const void* d_Linv, int64_t ldli, void* d_W, int64_t ldw, void* d_H,
+                             int64_t ldh);
+
 /* Full Hermitian eigendecomposition in place (cuSOLVER zheevd), ascending.
  * Stands in for linalg.py:292-323 `oracle_eig` / `_jacobi_raw` on the device. */
 int chfsi_heevd(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, double* h_w);

@@ -216,10 +216,8 @@ def _reduce_block(ab, lfac, linv=None):
         linv = dev.empty(n, n, ab.device)
         eng.trtri_lower(lfac.device_block(ab.device), linv)
     w = dev.empty(n, n, ab.device)
-    eng.zgemm("N", "N", n, n, n, 1.0, linv, ab, 0.0, w)
     h = dev.empty(n, n, ab.device)
-    eng.zgemm("N", "C", n, n, n, 1.0, w, linv, 0.0, h)
-    return h
+    return eng.reduce_to_standard(ab, linv, w, h)
 
 
 def back_transform(Y, L):

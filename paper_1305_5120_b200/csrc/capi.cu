@@ -63,6 +63,9 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
                     double lam_ref, const double2* H_host, long long ldh_host, double2* H,
                     long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
                     int panels, int* result_in_w);
+int reduce_to_standard(Handle* h, long long n, const double2* A, long long lda,
+                       const double2* Linv, long long ldli, double2* W, long long ldw,
+                       double2* H, long long ldh);
 int lanczos_bound(Handle* h, long long n, int k, const double2* H, long long ldh,
                   const double2* v0, double* alphas, double* betas, int* steps, double* bound);
 int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ldf,
@@ -372,6 +375,18 @@ int chfsi_cholesky(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, int* h_i
   if (info != 0) return OK;  // caller maps info > 0 to NotPositiveDefinite(pivot)
   CHFSI_TRY(clean_lower_factor(h, n, (double2*)d_A, lda));
   return OK;
+}
+
+int chfsi_reduce_to_standard(chfsi_handle_t h, int64_t n, const void* d_A, int64_t lda,
+                             const void* d_Linv, int64_t ldli, void* d_W, int64_t ldw, void* d_H,
+                             int64_t ldh) {
+  H_CHECK(h);
+  if (n < 0 || lda < n || ldli < n || ldw < n || ldh < n) {
+    set_error("reduce_to_standard: bad order or leading dimension");
+    return ERR_ARG;
+  }
+  return reduce_to_standard(h, n, (const double2*)d_A, lda, (const double2*)d_Linv, ldli,
+                            (double2*)d_W, ldw, (double2*)d_H, ldh);
 }
 
 int chfsi_trtri_lower(chfsi_handle_t h, int64_t n, const void* d_L, int64_t ldl, void* d_X,

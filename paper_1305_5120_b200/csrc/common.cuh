@@ -13,6 +13,8 @@
 namespace chfsi {
 
 enum Op : int { OP_N = 0, OP_C = 1 };  // OP_C = conjugate transpose
+// Triangular GEMM operands (zgemm `tri`): the zero blocks of the K range are skipped.
+enum Tri : int { TRI_NONE = 0, TRI_A_LOWER = 1, TRI_B_UPPER = 2, TRI_B_LOWER = 4 };
 
 // D(8x8) += A(8x4, row) * B(4x8, col), all f64. One SASS DMMA.8x8x4.
 // Fragment ownership (PTX ISA, m8n8k4 .f64):

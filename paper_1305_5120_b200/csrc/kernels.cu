@@ -378,10 +378,11 @@ static int trtri_rec(Handle* h, long long n, const double2* L, long long ldl, do
   CHFSI_TRY(trtri_rec(h, n1, L, ldl, X, ldx, tmp));
   CHFSI_TRY(trtri_rec(h, n2, L + n1 + n1 * ldl, ldl, X + n1 + n1 * ldx, ldx, tmp));
   // tmp(n2 x n1) = L21 * X11 ; X21 = -X22 * tmp ; X12 = 0
+  // (X11 and X22 are lower triangular: their zero blocks are skipped)
   CHFSI_TRY(zgemm(h, OP_N, OP_N, n2, n1, n1, make_double2(1.0, 0.0), L + n1, ldl, X, ldx,
-                  make_double2(0.0, 0.0), tmp, n2));
+                  make_double2(0.0, 0.0), tmp, n2, TRI_B_LOWER));
   CHFSI_TRY(zgemm(h, OP_N, OP_N, n2, n1, n2, make_double2(-1.0, 0.0), X + n1 + n1 * ldx, ldx,
-                  tmp, n2, make_double2(0.0, 0.0), X + n1, ldx));
+                  tmp, n2, make_double2(0.0, 0.0), X + n1, ldx, TRI_A_LOWER));
   CHFSI_CUDA(cudaMemset2DAsync(X + n1 * ldx, ldx * sizeof(double2), 0, n1 * sizeof(double2), n2,
                                h->stream));
   return OK;

@@ -539,6 +539,16 @@ int project_out(Handle* h, long long n, long long k, double2* F, long long ldf,
   return OK;
 }
 
+// core.py:172-188 `reduce_to_standard`: H = L^-1 A L^-H from the triangular inverse
+// Linv = L^-1 as two DMMA GEMMs that skip Linv's zero triangle (half the flops each):
+// W = Linv A (row tile m needs k <= m), H = W Linv^H (column tile j needs k <= j).
+int reduce_to_standard(Handle* h, long long n, const double2* A, long long lda,
+                       const double2* Linv, long long ldli, double2* W, long long ldw,
+                       double2* H, long long ldh) {
+  CHFSI_TRY(zgemm(h, OP_N, OP_N, n, n, n, ONE, Linv, ldli, A, lda, ZERO, W, ldw, TRI_A_LOWER));
+  return zgemm(h, OP_N, OP_C, n, n, n, ONE, W, ldw, Linv, ldli, ZERO, H, ldh, TRI_B_UPPER);
+}
+
 // core.py:318-330 `_rr_raw` plus the residual norms of core.py:477, with a single
 // host sync: Ritz values, residuals and the zheevd info come back together.
 // hq_ready: the caller already holds HQ = H Q (column-sharded multi-GPU path).

@@ -46,7 +46,18 @@ struct GemmParams {
   // (CUDA-graph replays of the filter reuse one captured launch sequence while the
   // Chebyshev coefficients change every outer iteration)
   const double* coef;
+  // Tri flags: A (op N) lower triangular -> row tile m0 needs k < m0 + BM; op(B) upper
+  // triangular -> column tile n0 needs k < n0 + BN; B (op N) lower triangular -> column
+  // tile n0 needs k >= n0. The longest tiles go first.
+  int tri;
 };
+
+__device__ __forceinline__ void tri_krange(const GemmParams& p, int m0, int n0, int bm, int bn,
+                                           int& kbeg, int& kend) {
+  if (p.tri & TRI_A_LOWER) kend = min(kend, m0 + bm);
+  if (p.tri & TRI_B_UPPER) kend = min(kend, n0 + bn);
+  if (p.tri & TRI_B_LOWER) kbeg = max(kbeg, n0);
+}
 
 __device__ __forceinline__ void filter_coef(const GemmParams& p, double& a, double& b, double& g) {
   if (p.coef != nullptr) {
@@ -69,6 +80,10 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, int b, int& mi,
   const int r = b - g * per_group;
   mi = first + r % gsize;
   ni = r / gsize;
+  // triangular operands: the tiles with the longest K range first (fewer idle SMs in
+  // the last wave)
+  if (p.tri & TRI_A_LOWER) mi = p.tiles_m - 1 - mi;
+  if (p.tri & TRI_B_UPPER) ni = p.tiles_n - 1 - ni;
 }
 
 template <int BM, int BK, int OPA>
@@ -111,6 +126,7 @@ zgemm_dmma_kernel(const GemmParams p) {
     kbeg = blockIdx.z * p.k_chunk;
     kend = min(p.K, kbeg + p.k_chunk);
   }
+  tri_krange(p, m0, n0, BM, BN, kbeg, kend);
   const int KT = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
 
   auto load_tile = [&](int kt, int stage) {

@@ -118,6 +118,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     kbeg = blockIdx.z * p.k_chunk;
     kend = min(p.K, kbeg + p.k_chunk);
   }
+  tri_krange(p, m0, n0, BM, BN, kbeg, kend);
   const int KT = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
 
   if (tid == 0) {

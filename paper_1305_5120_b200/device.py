@@ -258,6 +258,13 @@ class Engine:
             raise ContractViolation(f"zpotrf: illegal argument {-info.value}")
         return A
 
+    def reduce_to_standard(self, A, Linv, W, H):
+        """H = Linv A Linv^H (chfsi_reduce_to_standard); W is an n x n work block."""
+        n = rows(A)
+        _native.call("chfsi_reduce_to_standard", self.h, n, ptr(A), ld(A), ptr(Linv), ld(Linv),
+                     ptr(W), ld(W), ptr(H), ld(H))
+        return H
+
     def trtri_lower(self, L, X):
         _native.call("chfsi_trtri_lower", self.h, rows(L), ptr(L), ld(L), ptr(X), ld(X))
         return X

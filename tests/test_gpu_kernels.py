@@ -289,6 +289,45 @@ def test_cholesky_trtri_heevd(eng):
     assert np.max(np.abs(w - np.linalg.eigvalsh(h))) <= 1e-13 * np.max(np.abs(w))
 
 
+@pytest.mark.parametrize("cfg", [-1, 1, 3, 7, 10])
+@pytest.mark.parametrize("split", [0, 1, 3])
+def test_triangle_skipping_gemm_and_reduction(eng, cfg, split):
+    """Linv A (row tile m reads k < m + BM) and W Linv^H (column tile j reads k < j + BN)
+    skip Linv's zero triangle; the products equal the dense ones, including ragged
+    orders, forced configs and split-K chunks that fall entirely in the zero block."""
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    rng = np.random.default_rng(77 + cfg + 5 * split)
+    try:
+        assert lib.chfsi_gemm_override(cfg, split) == 0
+        for n in (1, 37, 130, 301):
+            a = crand(rng, n, n)
+            a = a + a.conj().T
+            linv = np.tril(crand(rng, n, n))
+            dA, dL = D.to_device(a, eng.device), D.to_device(linv, eng.device)
+            w, h = D.empty(n, n, eng.device), D.empty(n, n, eng.device)
+            eng.reduce_to_standard(dA, dL, w, h)
+            ref_w = linv @ a
+            ref_h = ref_w @ linv.conj().T
+            assert np.linalg.norm(D.to_host(w) - ref_w) <= 1e-13 * np.linalg.norm(ref_w), n
+            assert np.linalg.norm(D.to_host(h) - ref_h) <= 1e-13 * np.linalg.norm(ref_h), n
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
+def test_trtri_blocked_matches_inverse(eng):
+    """Recursive triangular inverse (its GEMMs skip the zero blocks of X11 / X22)."""
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(12)
+    for n in (255, 600, 1100):
+        lo = np.tril(crand(rng, n, n)) * 0.05 + np.diag(2.0 + rng.random(n))
+        x = D.empty(n, n, eng.device)
+        eng.trtri_lower(D.to_device(lo, eng.device), x)
+        got = D.to_host(x)
+        assert np.array_equal(np.triu(got, 1), np.zeros((n, n)))
+        assert np.linalg.norm(got @ lo - np.eye(n)) <= 1e-12 * n
+
+
 # every tile configuration and split factor the cost model can pick, on ragged shapes
 _NCFG = 11
 _TMA_FIRST = 7
