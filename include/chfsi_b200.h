@@ -54,6 +54,21 @@ int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_
                 const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
                 int64_t ldc);
 
+/* chfsi_zgemm with a triangular operand whose zero triangle holds zeros; the GEMM
+ * skips those blocks of the K range (half the work for a square factor). Replaces
+ * the ztrmm / ztrsm-via-inverse products of linalg.py:326-366 (`triangular_solve`,
+ * `trmm_adjoint`) and core.py:191-195 (`back_transform`). Flags (OR-able):
+ *   1  A lower triangular, opa = N, m == k      4  B lower triangular, opb = N, n == k
+ *   2  op(B) = L^H (L lower), opb = C, n == k   8  op(A) = L^H (L lower), opa = C, m == k */
+#define CHFSI_TRI_A_LOWER 1
+#define CHFSI_TRI_B_UPPER 2
+#define CHFSI_TRI_B_LOWER 4
+#define CHFSI_TRI_A_UPPER 8
+int chfsi_zgemm_tri(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_t k,
+                    double alpha_re, double alpha_im, const void* d_A, int64_t lda,
+                    const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
+                    int64_t ldc, int tri);
+
 /* Scaled degree-m Chebyshev filter p_m(H) Y, core.py:263-284 `_filter_raw`.
  * d_Y (n x k) is clobbered; the result is in d_W when *h_result_in_w == 1,
  * else in d_Y. Exactly `degree` fused GEMM launches (H streamed once each). */

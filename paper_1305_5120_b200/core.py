@@ -637,10 +637,11 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callb
     if Y0 is not None and not (isinstance(Y0, str) and Y0 == "random"):
         yb = Y0.device_block(d) if isinstance(Y0, VectorBlock) else to_block(_host_block(Y0), d)
         fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
-        eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd)
+        eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd,
+                  tri=eng.TRI_A_UPPER)
         y0 = VectorBlock(fwd)
     lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed, group=group,
                                   callback=callback)
     c = dev.empty(n, yv.s, d)
-    eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c)
+    eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c, tri=eng.TRI_A_UPPER)
     return lam, VectorBlock(c), report

@@ -14,7 +14,13 @@ namespace chfsi {
 
 enum Op : int { OP_N = 0, OP_C = 1 };  // OP_C = conjugate transpose
 // Triangular GEMM operands (zgemm `tri`): the zero blocks of the K range are skipped.
-enum Tri : int { TRI_NONE = 0, TRI_A_LOWER = 1, TRI_B_UPPER = 2, TRI_B_LOWER = 4 };
+enum Tri : int {
+  TRI_NONE = 0,
+  TRI_A_LOWER = 1,  // A (op N) lower triangular: row tile m0 needs k < m0 + BM
+  TRI_B_UPPER = 2,  // op(B) = L^H, L lower: column tile n0 needs k < n0 + BN
+  TRI_B_LOWER = 4,  // B (op N) lower triangular: column tile n0 needs k >= n0
+  TRI_A_UPPER = 8,  // op(A) = L^H, L lower: row tile m0 needs k >= m0
+};
 
 // D(8x8) += A(8x4, row) * B(4x8, col), all f64. One SASS DMMA.8x8x4.
 // Fragment ownership (PTX ISA, m8n8k4 .f64):

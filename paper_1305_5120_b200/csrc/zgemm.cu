@@ -483,6 +483,14 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
     set_error("zgemm: a lower-triangular B must be square and op N");
     return ERR_ARG;
   }
+  if ((tri & TRI_A_UPPER) && (opa != OP_C || M != K)) {
+    set_error("zgemm: an upper-triangular op(A) must be square and op C of a lower factor");
+    return ERR_ARG;
+  }
+  if (tri & ~(TRI_A_LOWER | TRI_B_UPPER | TRI_B_LOWER | TRI_A_UPPER)) {
+    set_error("zgemm: unknown tri flags");
+    return ERR_ARG;
+  }
   p.tri = tri;
   return launch(h, opa, opb, EPI_STORE, M, N, K, p);
 }

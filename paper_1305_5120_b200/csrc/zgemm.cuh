@@ -46,9 +46,7 @@ struct GemmParams {
   // (CUDA-graph replays of the filter reuse one captured launch sequence while the
   // Chebyshev coefficients change every outer iteration)
   const double* coef;
-  // Tri flags: A (op N) lower triangular -> row tile m0 needs k < m0 + BM; op(B) upper
-  // triangular -> column tile n0 needs k < n0 + BN; B (op N) lower triangular -> column
-  // tile n0 needs k >= n0. The longest tiles go first.
+  // Tri flags (common.cuh): K ranges of triangular operands; the longest tiles go first.
   int tri;
 };
 
@@ -57,6 +55,7 @@ __device__ __forceinline__ void tri_krange(const GemmParams& p, int m0, int n0, 
   if (p.tri & TRI_A_LOWER) kend = min(kend, m0 + bm);
   if (p.tri & TRI_B_UPPER) kend = min(kend, n0 + bn);
   if (p.tri & TRI_B_LOWER) kbeg = max(kbeg, n0);
+  if (p.tri & TRI_A_UPPER) kbeg = max(kbeg, m0);
 }
 
 __device__ __forceinline__ void filter_coef(const GemmParams& p, double& a, double& b, double& g) {
@@ -85,6 +84,7 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, int b, int& mi,
   if (p.tri & TRI_A_LOWER) mi = p.tiles_m - 1 - mi;
   if (p.tri & TRI_B_UPPER) ni = p.tiles_n - 1 - ni;
 }
+// (TRI_A_UPPER / TRI_B_LOWER: the low tiles are the long ones, already first)
 
 template <int BM, int BK, int OPA>
 struct ATile {

@@ -354,9 +354,11 @@ def oracle_eig(H, max_sweeps=30):
 
 
 def _factor_block(L):
+    """Device copy of a lower-triangular factor with a zero upper triangle: like the
+    reference's ztrsm/ztrmm (lower=1) only the lower triangle of a raw array is used."""
     if isinstance(L, LowerTriangularFactor):
         return L.device_block()
-    return dev.to_device(_asarray(L), default_device())
+    return dev.to_device(np.tril(_asarray(L)), default_device())
 
 
 def _inverse_factor(L):
@@ -390,10 +392,13 @@ def solve_triangular_device(L, xb, side="left", adjoint=False, linv=None):
     eng = engine(xb.device)
     m, n = dev.rows(xb), dev.cols(xb)
     out = dev.empty(m, n, xb.device)
+    # linv is lower triangular with a zero upper triangle: skip its zero blocks
     if side == "left":
-        eng.zgemm("C" if adjoint else "N", "N", m, n, m, 1.0, linv, xb, 0.0, out)
+        eng.zgemm("C" if adjoint else "N", "N", m, n, m, 1.0, linv, xb, 0.0, out,
+                  tri=eng.TRI_A_UPPER if adjoint else eng.TRI_A_LOWER)
     else:
-        eng.zgemm("N", "C" if adjoint else "N", m, n, n, 1.0, xb, linv, 0.0, out)
+        eng.zgemm("N", "C" if adjoint else "N", m, n, n, 1.0, xb, linv, 0.0, out,
+                  tri=eng.TRI_B_UPPER if adjoint else eng.TRI_B_LOWER)
     return out
 
 
@@ -407,6 +412,7 @@ def trmm_adjoint(L, X):
     xb = to_block(x2d)
     lb = _factor_block(L)
     out = dev.empty(dev.rows(xb), dev.cols(xb), xb.device)
-    engine(xb.device).zgemm("C", "N", ln, dev.cols(xb), ln, 1.0, lb, xb, 0.0, out)
+    eng = engine(xb.device)
+    eng.zgemm("C", "N", ln, dev.cols(xb), ln, 1.0, lb, xb, 0.0, out, tri=eng.TRI_A_UPPER)
     res = dev.to_host(out)
     return res[:, 0] if xh.ndim == 1 else res

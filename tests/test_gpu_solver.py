@@ -437,6 +437,29 @@ def test_linalg_dropin_semantics():
     assert np.array_equal(lf.entries, np.diag([2.0, 3.0]).astype(complex))
 
 
+@pytest.mark.parametrize("n", [5, 130, 700])
+def test_triangular_solve_and_trmm_use_only_the_lower_triangle(n):
+    """linalg.py:326-366: ztrsm / ztrmm with lower=1 read only the lower triangle of a raw
+    factor; the device versions (triangle-skipping GEMMs on L^-1 or L) must too."""
+    import paper_1305_5120_b200 as G
+    rng = np.random.default_rng(n)
+    lo = np.tril(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) * 0.1
+    lo[np.diag_indices(n)] = 1.0 + rng.random(n)
+    raw = lo + np.triu(rng.standard_normal((n, n)), 1) * 7.0  # garbage above the diagonal
+    x = rng.standard_normal((n, 9)) + 1j * rng.standard_normal((n, 9))
+    xr = rng.standard_normal((9, n)) + 1j * rng.standard_normal((9, n))
+    li = np.linalg.inv(lo)
+    cases = [(x, "left", False, li @ x), (x, "left", True, li.conj().T @ x),
+             (xr, "right", False, xr @ li), (xr, "right", True, xr @ li.conj().T)]
+    for fac in (raw, G.LowerTriangularFactor(lo)):
+        for blk, side, adj, ref in cases:
+            got = G.triangular_solve(fac, blk, side=side, adjoint=adj)
+            assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref), (side, adj)
+        got = G.trmm_adjoint(fac, x)
+        ref = lo.conj().T @ x
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
 def test_criterion7_report_csv_deterministic():
     """Reference criterion 7 (test_acceptance.py:199-227): repeated runs give identical
     non-timing report columns, eigenvalues and vectors."""
