@@ -54,12 +54,15 @@ int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_
                 const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
                 int64_t ldc);
 
-/* chfsi_zgemm with a triangular operand whose zero triangle holds zeros; the GEMM
+/* chfsi_zgemm with one triangular operand whose zero triangle holds zeros; the GEMM
  * skips those blocks of the K range (half the work for a square factor). Replaces
  * the ztrmm / ztrsm-via-inverse products of linalg.py:326-366 (`triangular_solve`,
- * `trmm_adjoint`) and core.py:191-195 (`back_transform`). Flags (OR-able):
- *   1  A lower triangular, opa = N, m == k      4  B lower triangular, opb = N, n == k
- *   2  op(B) = L^H (L lower), opb = C, n == k   8  op(A) = L^H (L lower), opa = C, m == k */
+ * `trmm_adjoint`) and core.py:191-195 (`back_transform`). Flags (one of):
+ *   1  A lower triangular (opa = N)             4  B lower triangular (opb = N)
+ *   2  op(B) = L^H, L lower (opb = C)           8  op(A) = L^H, L lower (opa = C)
+ * The factor has order k; C holds its rows (flags 1, 8) or columns (2, 4)
+ * [tri_offset, tri_offset + m or n): 0 for a whole factor, the shard start when a
+ * rank computes a column range of L^-1 A L^-H (distributed.reduce_sharded). */
 #define CHFSI_TRI_A_LOWER 1
 #define CHFSI_TRI_B_UPPER 2
 #define CHFSI_TRI_B_LOWER 4
@@ -67,7 +70,7 @@ int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_
 int chfsi_zgemm_tri(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_t k,
                     double alpha_re, double alpha_im, const void* d_A, int64_t lda,
                     const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
-                    int64_t ldc, int tri);
+                    int64_t ldc, int tri, int64_t tri_offset);
 
 /* Scaled degree-m Chebyshev filter p_m(H) Y, core.py:263-284 `_filter_raw`.
  * d_Y (n x k) is clobbered; the result is in d_W when *h_result_in_w == 1,

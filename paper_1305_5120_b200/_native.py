@@ -40,8 +40,8 @@ SIGNATURES = {
     "chfsi_launch_count": (ctypes.c_longlong, [_c_void_p, _int]),
     "chfsi_zgemm": (_int, [_c_void_p, _int, _int, _i64, _i64, _i64, _dbl, _dbl, _c_void_p, _i64,
                             _c_void_p, _i64, _dbl, _dbl, _c_void_p, _i64]),
-    "chfsi_zgemm_tri": (_int, [_c_void_p, _int, _int, _i64, _i64, _i64, _dbl, _dbl, _c_void_p, _i64,
-                            _c_void_p, _i64, _dbl, _dbl, _c_void_p, _i64, _int]),
+    "chfsi_zgemm_tri": (_int, [_c_void_p, _int, _int, _i64, _i64, _i64, _dbl, _dbl, _c_void_p,
+                                _i64, _c_void_p, _i64, _dbl, _dbl, _c_void_p, _i64, _int, _i64]),
     "chfsi_filter": (_int, [_c_void_p, _i64, _i64, _int, _dbl, _dbl, _dbl, _c_void_p, _i64,
                              _c_void_p, _i64, _c_void_p, _i64, _pint]),
     "chfsi_filter_streamed": (_int, [_c_void_p, _i64, _i64, _int, _dbl, _dbl, _dbl, _c_void_p,

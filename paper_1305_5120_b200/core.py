@@ -632,7 +632,13 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callb
         ab = dev.to_device(ah, d)
     n = dev.rows(ab)
     eng = engine(d)
-    hm = HermitianDenseMatrix(_reduce_block(ab, lfac, linv), rtol=1e-8)
+    from .distributed import reduce_sharded, world_info
+    if group is not None and world_info(group)[1] > 1:
+        # column-sharded reduction + all-gather: every rank ends with the same H
+        hb = reduce_sharded(eng, ab, linv, group)
+    else:
+        hb = _reduce_block(ab, lfac, linv)
+    hm = HermitianDenseMatrix(hb, rtol=1e-8)
     y0 = Y0
     if Y0 is not None and not (isinstance(Y0, str) and Y0 == "random"):
         yb = Y0.device_block(d) if isinstance(Y0, VectorBlock) else to_block(_host_block(Y0), d)

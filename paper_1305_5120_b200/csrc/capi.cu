@@ -251,14 +251,15 @@ int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_
 int chfsi_zgemm_tri(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_t k,
                     double alpha_re, double alpha_im, const void* d_A, int64_t lda,
                     const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,
-                    int64_t ldc, int tri) {
+                    int64_t ldc, int tri, int64_t tri_offset) {
   H_CHECK(h);
   if (m < 0 || n < 0 || k < 0) {
     set_error("chfsi_zgemm_tri: negative dimension");
     return ERR_ARG;
   }
   return zgemm(h, opa, opb, m, n, k, c2(alpha_re, alpha_im), (const double2*)d_A, lda,
-               (const double2*)d_B, ldb, c2(beta_re, beta_im), (double2*)d_C, ldc, tri);
+               (const double2*)d_B, ldb, c2(beta_re, beta_im), (double2*)d_C, ldc, tri,
+               tri_offset);
 }
 
 int chfsi_filter(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a, double b,

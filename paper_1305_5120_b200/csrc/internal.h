@@ -110,11 +110,11 @@ double* pinned(Handle* h, size_t bytes);
 
 // ---- GEMM (zgemm.cu) ----
 // C = alpha op(A) op(B) + beta C, complex128 column-major.
-// tri: TRI_A_LOWER (A lower triangular, op N) | TRI_B_UPPER (op(B) = L^H, L lower):
-// the zero blocks of the K range are skipped (zgemm.cuh).
+// tri: one triangular operand (common.cuh Tri flags); the zero blocks of the K range
+// are skipped. tri_off: first row (A flags) / column (B flags) of C in the factor.
 int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, double2 alpha,
           const double2* A, long long lda, const double2* B, long long ldb, double2 beta,
-          double2* C, long long ldc, int tri = 0);
+          double2* C, long long ldc, int tri = 0, long long tri_off = 0);
 // One fused Chebyshev degree step: C = alpha*A*Y1 + beta*Y1 + gamma*Y0 (Y0 may be null,
 // C may alias Y0). A is M x M, Y1/Y0/C are M x N.
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,

@@ -460,7 +460,7 @@ int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, lo
 
 int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, double2 alpha,
           const double2* A, long long lda, const double2* B, long long ldb, double2 beta,
-          double2* C, long long ldc, int tri) {
+          double2* C, long long ldc, int tri, long long tri_off) {
   if ((opa != OP_N && opa != OP_C) || (opb != OP_N && opb != OP_C)) {
     set_error("zgemm: op must be 0 (N) or 1 (C)");
     return ERR_ARG;
@@ -471,27 +471,25 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
   p.C = C; p.ldc = ldc;
   p.alpha = alpha; p.beta = beta;
   p.Y0 = nullptr; p.ld0 = 0; p.gamma = 0.0;
-  if ((tri & TRI_A_LOWER) && (opa != OP_N || M != K)) {
-    set_error("zgemm: a lower-triangular A must be square and op N");
-    return ERR_ARG;
-  }
-  if ((tri & TRI_B_UPPER) && (opb != OP_C || N != K)) {
-    set_error("zgemm: an upper-triangular op(B) must be square and op C of a lower factor");
-    return ERR_ARG;
-  }
-  if ((tri & TRI_B_LOWER) && (opb != OP_N || N != K)) {
-    set_error("zgemm: a lower-triangular B must be square and op N");
-    return ERR_ARG;
-  }
-  if ((tri & TRI_A_UPPER) && (opa != OP_C || M != K)) {
-    set_error("zgemm: an upper-triangular op(A) must be square and op C of a lower factor");
-    return ERR_ARG;
-  }
+  // a triangular operand is square in the full factor; C covers rows (A flags) or
+  // columns (B flags) [tri_off, tri_off + M or N) of it
+  const bool a_tri = tri & (TRI_A_LOWER | TRI_A_UPPER), b_tri = tri & (TRI_B_LOWER | TRI_B_UPPER);
   if (tri & ~(TRI_A_LOWER | TRI_B_UPPER | TRI_B_LOWER | TRI_A_UPPER)) {
     set_error("zgemm: unknown tri flags");
     return ERR_ARG;
   }
+  if ((a_tri && b_tri) || tri_off < 0 || (a_tri && tri_off + M > K) ||
+      (b_tri && tri_off + N > K)) {
+    set_error("zgemm: tri flags need one triangular operand of order K covering C");
+    return ERR_ARG;
+  }
+  if (((tri & TRI_A_LOWER) && opa != OP_N) || ((tri & TRI_A_UPPER) && opa != OP_C) ||
+      ((tri & TRI_B_LOWER) && opb != OP_N) || ((tri & TRI_B_UPPER) && opb != OP_C)) {
+    set_error("zgemm: tri flag does not match the operand's op (lower: N, L^H: C)");
+    return ERR_ARG;
+  }
   p.tri = tri;
+  p.tri_off = (int)tri_off;
   return launch(h, opa, opb, EPI_STORE, M, N, K, p);
 }
 

@@ -47,15 +47,18 @@ struct GemmParams {
   // Chebyshev coefficients change every outer iteration)
   const double* coef;
   // Tri flags (common.cuh): K ranges of triangular operands; the longest tiles go first.
+  // tri_off: global index of row/column 0 of C inside the triangular factor (a column
+  // shard of L^-1 A L^-H multiplies by rows [tri_off, tri_off + N) of L^-1).
   int tri;
+  int tri_off;
 };
 
 __device__ __forceinline__ void tri_krange(const GemmParams& p, int m0, int n0, int bm, int bn,
                                            int& kbeg, int& kend) {
-  if (p.tri & TRI_A_LOWER) kend = min(kend, m0 + bm);
-  if (p.tri & TRI_B_UPPER) kend = min(kend, n0 + bn);
-  if (p.tri & TRI_B_LOWER) kbeg = max(kbeg, n0);
-  if (p.tri & TRI_A_UPPER) kbeg = max(kbeg, m0);
+  if (p.tri & TRI_A_LOWER) kend = min(kend, p.tri_off + m0 + bm);
+  if (p.tri & TRI_B_UPPER) kend = min(kend, p.tri_off + n0 + bn);
+  if (p.tri & TRI_B_LOWER) kbeg = max(kbeg, p.tri_off + n0);
+  if (p.tri & TRI_A_UPPER) kbeg = max(kbeg, p.tri_off + m0);
 }
 
 __device__ __forceinline__ void filter_coef(const GemmParams& p, double& a, double& b, double& g) {

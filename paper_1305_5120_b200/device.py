@@ -132,9 +132,10 @@ class Engine:
     # triangular-operand flags of chfsi_zgemm_tri (include/chfsi_b200.h)
     TRI_A_LOWER, TRI_B_UPPER, TRI_B_LOWER, TRI_A_UPPER = 1, 2, 4, 8
 
-    def zgemm(self, opa, opb, m, n, k, alpha, A, B, beta, C, tri=0):
+    def zgemm(self, opa, opb, m, n, k, alpha, A, B, beta, C, tri=0, tri_offset=0):
         """C = alpha op(A) op(B) + beta C on column-major blocks (op: 'N' or 'C').
-        ``tri``: triangular-operand flags; the zero blocks of the K range are skipped."""
+        ``tri``: triangular-operand flag (the zero blocks of the K range are skipped);
+        ``tri_offset``: first row/column of C inside the triangular factor."""
         oa = 0 if opa == "N" else 1
         ob = 0 if opb == "N" else 1
         alpha = complex(alpha)
@@ -142,7 +143,7 @@ class Engine:
         if tri:
             _native.call("chfsi_zgemm_tri", self.h, oa, ob, m, n, k, alpha.real, alpha.imag,
                          ptr(A), ld(A), ptr(B), ld(B), beta.real, beta.imag, ptr(C), ld(C),
-                         int(tri))
+                         int(tri), int(tri_offset))
         else:
             _native.call("chfsi_zgemm", self.h, oa, ob, m, n, k, alpha.real, alpha.imag,
                          ptr(A), ld(A), ptr(B), ld(B), beta.real, beta.imag, ptr(C), ld(C))

@@ -16,14 +16,21 @@ import torch.distributed as dist
 
 
 class ColumnShards:
-    """Contiguous split of k columns over ``world`` ranks."""
+    """Contiguous split of k columns over ``world`` ranks (default: the reference's
+    worker bounds; ``bounds`` may give any non-decreasing split of [0, k])."""
 
-    def __init__(self, k, world):
+    def __init__(self, k, world, bounds=None):
         if k < 0 or world < 1:
             raise ValueError("need k >= 0 and world >= 1")
         self.k = int(k)
         self.world = int(world)
-        self.bounds = [(self.k * i) // self.world for i in range(self.world + 1)]
+        if bounds is None:
+            bounds = [(self.k * i) // self.world for i in range(self.world + 1)]
+        bounds = [int(b) for b in bounds]
+        if (len(bounds) != self.world + 1 or bounds[0] != 0 or bounds[-1] != self.k
+                or any(b1 < b0 for b0, b1 in zip(bounds, bounds[1:]))):
+            raise ValueError(f"bad shard bounds {bounds} for k={k}, world={world}")
+        self.bounds = bounds
         self.widths = [self.bounds[i + 1] - self.bounds[i] for i in range(self.world)]
         self.padded = max(self.widths) if self.widths else 0
 
@@ -155,3 +162,40 @@ class ShardedPhases:
         if hi > lo:
             eng.zgemm("N", "N", n, hi - lo, n, 1.0, H, Q[lo:hi], 0.0, HQ[lo:hi])
         return self._gather(sh, HQ[lo:hi], HQ[:k])
+
+
+def reduction_bounds(n, world, align=64):
+    """Column split of H = L^-1 A L^-H with equal work per rank. Column c costs
+    n (c + 1) complex MACs in X = A L^-H[:, c] (row c of L^-1 has c + 1 nonzeros) plus
+    n^2 / 2 in L^-1 X (triangle-skipping), so the cumulative cost is
+    F(c) ~ c^2 / 2 + n c / 2 and rank p starts at F^-1(p F(n) / world) =
+    n (sqrt(1 + 8 p / world) - 1) / 2, rounded to ``align`` columns."""
+    out = [0]
+    for p in range(1, world):
+        c = n * ((1.0 + 8.0 * p / world) ** 0.5 - 1.0) / 2.0
+        c = int(round(c / align)) * align
+        out.append(min(max(c, out[-1]), n))
+    out.append(n)
+    return out
+
+
+def reduce_sharded(eng, A, Linv, group=None):
+    """H = L^-1 A L^-H column-sharded over the ranks of ``group`` (SURVEY.md section
+    8f item 2): rank p computes X_p = A (L^-1[c_p, :])^H and H[:, c_p] = L^-1 X_p with
+    triangle-skipping DMMA GEMMs (chfsi_zgemm_tri with the shard offset), then the
+    column slabs are all-gathered (NCCL) so every rank holds H. Blocks are (cols, rows)
+    tensors; A and Linv are replicated."""
+    from . import device as dev
+    rank, world = world_info(group)
+    n = dev.rows(A)
+    sh = ColumnShards(n, world, reduction_bounds(n, world))
+    lo, hi = sh.range(rank)
+    w = hi - lo
+    x = dev.empty(n, w, A.device)
+    hp = dev.empty(n, w, A.device)
+    if w:
+        # op(B) = (rows lo..hi of L^-1)^H: a (cols, rows) view of those rows, ld = n
+        eng.zgemm("N", "C", n, w, n, 1.0, A, Linv[:, lo:hi], 0.0, x,
+                  tri=eng.TRI_B_UPPER, tri_offset=lo)
+        eng.zgemm("N", "N", n, w, n, 1.0, Linv, x, 0.0, hp, tri=eng.TRI_A_LOWER)
+    return sh.gather_block(hp, group)

@@ -76,6 +76,49 @@ def _sharded_filter(rank, world, port):
         dist.destroy_process_group()
 
 
+def _sharded_reduction_math(rank, world, port):
+    """Column-sharded L^-1 A L^-H (distributed.reduce_sharded's decomposition) with numpy
+    as the per-rank compute and the real balanced-bounds gather."""
+    _init(rank, world, port)
+    from paper_1305_5120_b200.distributed import ColumnShards, reduction_bounds
+    try:
+        n = 200
+        rng = np.random.default_rng(4)
+        a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        a = a + a.conj().T
+        linv = np.tril(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+        sh = ColumnShards(n, world, reduction_bounds(n, world, align=8))
+        lo, hi = sh.range(rank)
+        x = a @ linv[lo:hi, :].conj().T          # A (L^-1[c_p, :])^H
+        hp = linv @ x                              # H[:, c_p]
+        got = sh.gather_block(torch.from_numpy(np.ascontiguousarray(hp.T))).numpy().T
+        ref = linv @ a @ linv.conj().T
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_reduction_decomposition():
+    mp.spawn(_sharded_reduction_math, args=(2, _free_port()), nprocs=2, join=True)
+
+
+def test_reduction_bounds_balance_work():
+    """Equal work per rank for X = A L^-H[:, c] (cost ~ c) plus L^-1 X (cost ~ n / 2)."""
+    from paper_1305_5120_b200.distributed import ColumnShards, reduction_bounds
+    n = 20000
+    for world in (1, 2, 4, 8):
+        b = reduction_bounds(n, world)
+        assert b[0] == 0 and b[-1] == n and all(x % 64 == 0 for x in b[:-1])
+        assert all(b1 > b0 for b0, b1 in zip(b, b[1:]))
+        cost = [sum(c + n / 2 for c in range(b[i], b[i + 1])) for i in range(world)]
+        assert max(cost) / (sum(cost) / world) < 1.02
+        ColumnShards(n, world, b)
+    with pytest.raises(ValueError):
+        ColumnShards(10, 2, [0, 6, 5])
+    with pytest.raises(ValueError):
+        ColumnShards(10, 2, [0, 5])
+
+
 def test_column_shards_single_process():
     from paper_1305_5120_b200.distributed import ColumnShards
     sh = ColumnShards(10, 3)
@@ -125,3 +168,60 @@ def test_gloo_world2_sharded_solver_matches_single(tmp_path):
     assert np.max(np.abs(r0["lam"] - lam) / np.abs(lam)) <= 1e-10
     assert O.largest_angle_sine(r0["v"], v.entries) < 1e-8
     assert np.max(np.abs(r0["lam"] - lam_true[:30]) / np.abs(lam_true[:30])) <= 1e-10
+
+
+def _gapped_pencil_a(n, nev=20):
+    rng = np.random.default_rng(31)
+    ev = np.concatenate([np.sort(rng.uniform(0.0, 4.0, nev)), rng.uniform(6.0, 10.0, n - nev)])
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    a = (q * ev) @ q.conj().T
+    return (a + a.conj().T) / 2.0
+
+
+def _sharded_generalized(rank, world, port, out_dir):
+    _init(rank, world, port)
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.distributed import reduce_sharded
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        eng = D.Engine.get(dev)
+        n = 390
+        a = _gapped_pencil_a(n)
+        rng = np.random.default_rng(32)
+        bm = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        s = np.eye(n) + 0.1 * (bm.conj().T @ bm) / np.linalg.norm(bm.conj().T @ bm, 2)
+        lf = G.cholesky_factor(s)
+        linv = D.empty(n, n, dev)
+        eng.trtri_lower(lf.device_block(), linv)
+        h = reduce_sharded(eng, D.to_device(a, dev), linv, dist.group.WORLD)
+        cfg = G.SolverConfig(nev=20, buffer=6, degree=12, max_outer_iters=3000)
+        lam, c, rep = G.solve_generalized(a, s, None, cfg, seed=3, group=dist.group.WORLD)
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), h=D.to_host(h), lam=lam, c=c.entries)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_sharded_generalized_matches_single(tmp_path):
+    """solve_generalized(group=) with the column-sharded reduction (2 ranks on cuda:0,
+    gloo host staging) equals the single-process reduction and solve."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    mp.spawn(_sharded_generalized, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    g0, g1 = np.load(tmp_path / "g0.npz"), np.load(tmp_path / "g1.npz")
+    assert np.array_equal(g0["h"], g1["h"]) and np.array_equal(g0["lam"], g1["lam"])
+    n = 390
+    a = _gapped_pencil_a(n)
+    rng = np.random.default_rng(32)
+    bm = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    s = np.eye(n) + 0.1 * (bm.conj().T @ bm) / np.linalg.norm(bm.conj().T @ bm, 2)
+    lf = G.cholesky_factor(s)
+    href = G.reduce_to_standard(a, lf).entries
+    # reduce_to_standard symmetrises; the raw sharded product is Hermitian to rounding
+    assert np.linalg.norm(g0["h"] - href) <= 1e-13 * np.linalg.norm(href)
+    cfg = G.SolverConfig(nev=20, buffer=6, degree=12, max_outer_iters=3000)
+    lam, c, rep = G.solve_generalized(a, s, None, cfg, seed=3)
+    assert np.max(np.abs(g0["lam"] - lam) / np.abs(lam)) <= 1e-10
+    assert O.largest_angle_sine(g0["c"], c.entries) < 1e-8
