@@ -632,8 +632,9 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callb
         ab = dev.to_device(ah, d)
     n = dev.rows(ab)
     eng = engine(d)
-    from .distributed import reduce_sharded, world_info
-    if group is not None and world_info(group)[1] > 1:
+    from .distributed import reduce_sharded, upper_apply_sharded, world_info
+    sharded = group is not None and world_info(group)[1] > 1
+    if sharded:
         # column-sharded reduction + all-gather: every rank ends with the same H
         hb = reduce_sharded(eng, ab, linv, group)
     else:
@@ -642,12 +643,21 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callb
     y0 = Y0
     if Y0 is not None and not (isinstance(Y0, str) and Y0 == "random"):
         yb = Y0.device_block(d) if isinstance(Y0, VectorBlock) else to_block(_host_block(Y0), d)
-        fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
-        eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd,
-                  tri=eng.TRI_A_UPPER)
+        # forward map y = L^H c (core.py:565)
+        if sharded:
+            fwd = upper_apply_sharded(eng, lfac.device_block(), yb, group)
+        else:
+            fwd = dev.empty(dev.rows(yb), dev.cols(yb), d)
+            eng.zgemm("C", "N", n, dev.cols(yb), n, 1.0, lfac.device_block(), yb, 0.0, fwd,
+                      tri=eng.TRI_A_UPPER)
         y0 = VectorBlock(fwd)
     lam, yv, report = chfsi_solve(hm, y0, config, prior=prior, seed=seed, group=group,
                                   callback=callback)
-    c = dev.empty(n, yv.s, d)
-    eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c, tri=eng.TRI_A_UPPER)
+    # back-transform C = L^-H Y (core.py:191-195)
+    if sharded:
+        c = upper_apply_sharded(eng, linv, yv.device_block(d), group)
+    else:
+        c = dev.empty(n, yv.s, d)
+        eng.zgemm("C", "N", n, yv.s, n, 1.0, linv, yv.device_block(d), 0.0, c,
+                  tri=eng.TRI_A_UPPER)
     return lam, VectorBlock(c), report

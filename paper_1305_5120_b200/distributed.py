@@ -199,3 +199,19 @@ def reduce_sharded(eng, A, Linv, group=None):
                   tri=eng.TRI_B_UPPER, tri_offset=lo)
         eng.zgemm("N", "N", n, w, n, 1.0, Linv, x, 0.0, hp, tri=eng.TRI_A_LOWER)
     return sh.gather_block(hp, group)
+
+
+def upper_apply_sharded(eng, F, Y, group=None):
+    """F^H Y for a lower-triangular F (L for the forward map y = L^H c, L^-1 for the
+    back-transform c = L^-H y) with the columns of the replicated block Y split over
+    the ranks: each rank multiplies its columns (triangle-skipping GEMM), then the
+    results are all-gathered so every rank holds the full product."""
+    from . import device as dev
+    rank, world = world_info(group)
+    n, k = dev.rows(Y), dev.cols(Y)
+    sh = ColumnShards(k, world)
+    lo, hi = sh.range(rank)
+    part = dev.empty(n, hi - lo, Y.device)
+    if hi > lo:
+        eng.zgemm("C", "N", n, hi - lo, n, 1.0, F, Y[lo:hi], 0.0, part, tri=eng.TRI_A_UPPER)
+    return sh.gather_block(part, group)

@@ -178,6 +178,11 @@ def _gapped_pencil_a(n, nev=20):
     return (a + a.conj().T) / 2.0
 
 
+def _start_block(n, k):
+    rng = np.random.default_rng(5)
+    return rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+
+
 def _sharded_generalized(rank, world, port, out_dir):
     _init(rank, world, port)
     import paper_1305_5120_b200 as G
@@ -198,7 +203,11 @@ def _sharded_generalized(rank, world, port, out_dir):
         h = reduce_sharded(eng, D.to_device(a, dev), linv, dist.group.WORLD)
         cfg = G.SolverConfig(nev=20, buffer=6, degree=12, max_outer_iters=3000)
         lam, c, rep = G.solve_generalized(a, s, None, cfg, seed=3, group=dist.group.WORLD)
-        np.savez(os.path.join(out_dir, f"g{rank}.npz"), h=D.to_host(h), lam=lam, c=c.entries)
+        # explicit start block: exercises the sharded forward map y = L^H c
+        y0 = _start_block(n, 26)
+        lam2, c2, _ = G.solve_generalized(a, s, y0, cfg, seed=3, group=dist.group.WORLD)
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), h=D.to_host(h), lam=lam, c=c.entries,
+                 lam2=lam2, c2=c2.entries)
     finally:
         dist.destroy_process_group()
 
@@ -225,3 +234,7 @@ def test_gloo_world2_sharded_generalized_matches_single(tmp_path):
     lam, c, rep = G.solve_generalized(a, s, None, cfg, seed=3)
     assert np.max(np.abs(g0["lam"] - lam) / np.abs(lam)) <= 1e-10
     assert O.largest_angle_sine(g0["c"], c.entries) < 1e-8
+    lam2, c2, _ = G.solve_generalized(a, s, _start_block(n, 26), cfg, seed=3)
+    assert np.array_equal(g0["lam2"], g1["lam2"])
+    assert np.max(np.abs(g0["lam2"] - lam2) / np.abs(lam2)) <= 1e-10
+    assert O.largest_angle_sine(g0["c2"], c2.entries) < 1e-8
