@@ -467,33 +467,30 @@ def committed_traffic(n, k):
 
 
 def e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up, lam_ref, dev, steps=2):
-    """N-GPU e2e: every rank runs the public chebyshev_filter on its column shard from
-    pinned host H / Y (H2D inside), the filtered shards are all-gathered (NCCL), and
-    rank 0 copies the full filtered block back to the host. Time = max over ranks."""
+    """N-GPU e2e through the public API: every rank calls
+    chebyshev_filter(H, Y, spec, group=WORLD) on the same pinned host H / Y; inside,
+    each rank uploads one column slab of H (all-gathered over NVLink) and its own
+    column shard of Y, filters it and all-gathers the result; rank 0 then reads the
+    full filtered block back to the host. Time = max over ranks."""
     import torch
     import torch.distributed as dist
 
     import paper_1305_5120_b200 as G
     from paper_1305_5120_b200 import device as D
     n, k, m = args.n, args.k, args.degree
-    lo, hi = shards.range(rank)
     h_pin = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
     h_pin.copy_(H)
-    y_pin = torch.empty((hi - lo, n), dtype=torch.complex128, pin_memory=True)
-    y_pin.copy_(Yfull[lo:hi])
+    y_pin = torch.empty((k, n), dtype=torch.complex128, pin_memory=True)
+    y_pin.copy_(Yfull)
     h_np, y_np = h_pin.numpy().T, y_pin.numpy().T
     spec = G.FilterSpec(degree=m, a=a_edge, b=b_up, lam_ref=lam_ref)
-    gathered = torch.empty((shards.padded * world, n), dtype=torch.complex128, device=dev)
-    full = torch.empty((k, n), dtype=torch.complex128, device=dev)
     d2h = 0
 
     def one():
         nonlocal d2h
-        out = G.chebyshev_filter(h_np, y_np, spec)
-        shards.all_gather(out.device_block(), gathered)
-        shards.compact(gathered, full)
+        out = G.chebyshev_filter(h_np, y_np, spec, group=dist.group.WORLD)
         if rank == 0:
-            d2h = D.to_host(full).nbytes
+            d2h = D.to_host(out.device_block()).nbytes
 
     one()
     torch.cuda.synchronize()
@@ -505,9 +502,10 @@ def e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up, lam_ref, 
     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     return {"value": 8.0 * n * n * k * m * steps / float(dt) / 1e12, "unit": UNIT,
-            "h2d_bytes_per_step": int(world * 16 * n * n + 16 * n * k),
+            "h2d_bytes_per_step": int(16 * n * n + 16 * n * k),
             "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "path": "per rank chebyshev_filter(H, Y_shard, FilterSpec) + NCCL all-gather; "
+            "path": "chebyshev_filter(H, Y, FilterSpec, group=WORLD): per-rank H slab upload + "
+                    "NCCL all-gather of H, Y column shards, NCCL all-gather of the result; "
                     "rank 0 VectorBlock -> host"}
 
 

@@ -253,8 +253,14 @@ def _lanczos(hm, k, rng):
     return bound
 
 
-def chebyshev_filter(H, Y, spec):
-    """p_m(H) Y with the scaled Chebyshev recurrence (core.py:287-311)."""
+def chebyshev_filter(H, Y, spec, *, group=None):
+    """p_m(H) Y with the scaled Chebyshev recurrence (core.py:287-311).
+
+    ``group`` (keyword-only, B200 extension): a torch.distributed process group with
+    one process per GPU. Every rank passes the same H and Y; a host H is uploaded as
+    one column slab per rank and all-gathered over NVLink, each rank filters its
+    contiguous column range of Y, and the filtered shards are all-gathered, so every
+    rank returns the full p_m(H) Y."""
     if not isinstance(spec, FilterSpec):
         if all(hasattr(spec, f) for f in ("degree", "a", "b", "lam_ref")):
             spec = FilterSpec(spec.degree, spec.a, spec.b, spec.lam_ref)
@@ -265,6 +271,10 @@ def chebyshev_filter(H, Y, spec):
             f"lam_ref = {spec.lam_ref} lies inside the unwanted interval [{spec.a}, {spec.b}]; "
             f"wanted and unwanted intervals overlap (a larger buffer improves the "
             f"lambda_nev+1 estimate)")
+    if group is not None:
+        from .distributed import world_info
+        if world_info(group)[1] > 1:
+            return _filter_sharded(H, Y, spec, group)
     host_h = _streamable_host(H)
     if host_h is not None:
         return _filter_streamed(host_h, Y, spec)
@@ -327,6 +337,53 @@ def _filter_streamed(host_h, Y, spec):
                                          spec.lam_ref)
     _count_products(spec.degree * dev.cols(yb))
     return VectorBlock(out)
+
+
+def _filter_sharded(H, Y, spec, group):
+    """chebyshev_filter over the ranks of ``group`` (column-separable recurrence,
+    core.py:276-283): H replicated (host slabs + all-gather), Y's columns sharded."""
+    from .distributed import ColumnShards, replicate_from_host, world_info
+    rank, world = world_info(group)
+    device = default_device()
+    if isinstance(H, HermitianDenseMatrix):
+        hb = H.device_block(device)
+    elif isinstance(H, torch.Tensor):
+        hb = H
+    else:
+        if hasattr(H, "entries") and not isinstance(H, (VectorBlock, LowerTriangularFactor)):
+            H = H.entries
+        a = np.asarray(H)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ContractViolation(f"expected a square matrix, got shape {a.shape}")
+        a = np.asfortranarray(a, dtype=np.complex128)
+        hb = replicate_from_host(torch.from_numpy(a.T), device, group)
+    n = dev.rows(hb)
+    if isinstance(Y, VectorBlock):
+        yfull = Y.device_block(device)
+        k = dev.cols(yfull)
+        if dev.rows(yfull) != n:
+            raise ContractViolation(f"filter operand mismatch: H is {(n, n)}, Y has {dev.rows(yfull)} rows")
+        sh = ColumnShards(k, world)
+        lo, hi = sh.range(rank)
+        yb = yfull[lo:hi].clone()
+    else:
+        y = _host_block(Y)
+        y2d = y if y.ndim == 2 else y.reshape(-1, 1)
+        if y2d.shape[0] != n:
+            raise ContractViolation(
+                f"filter operand mismatch: H is {(n, n)}, Y has {y2d.shape[0]} rows")
+        k = y2d.shape[1]
+        sh = ColumnShards(k, world)
+        lo, hi = sh.range(rank)
+        yb = dev.to_device(y2d[:, lo:hi], device)
+    if hi > lo:
+        w = torch.empty_like(yb)
+        out = engine(device).filter(hb, yb, w, spec.degree, spec.a, spec.b, spec.lam_ref)
+    else:
+        out = yb
+    full = sh.gather_block(out, group)
+    _count_products(spec.degree * k)
+    return VectorBlock(full)
 
 
 def rayleigh_ritz(H, Q):

@@ -79,6 +79,9 @@ class ColumnShards:
     def gather_block(self, local, group=None):
         """Convenience: full (k, n) block from every rank's shard."""
         n = local.shape[1]
+        if self.padded * self.world == self.k:  # equal shards: gather in place
+            out = torch.empty((self.k, n), dtype=local.dtype, device=local.device)
+            return self.all_gather(local, out, group)
         g = torch.empty((self.padded * self.world, n), dtype=local.dtype, device=local.device)
         self.all_gather(local, g, group)
         out = torch.empty((self.k, n), dtype=local.dtype, device=local.device)
@@ -215,3 +218,16 @@ def upper_apply_sharded(eng, F, Y, group=None):
     if hi > lo:
         eng.zgemm("C", "N", n, hi - lo, n, 1.0, F, Y[lo:hi], 0.0, part, tri=eng.TRI_A_UPPER)
     return sh.gather_block(part, group)
+
+
+def replicate_from_host(host, device, group=None):
+    """Every rank of ``group`` gets the full (cols, rows) block ``host`` (a CPU tensor,
+    ideally pinned) on ``device``: rank p uploads only its column slab and the slabs
+    are all-gathered (NCCL over NVLink), so each rank moves 1/N of the bytes over
+    PCIe instead of all of them (c4: 0.8 GB instead of 6.4 GB per GPU at N = 8)."""
+    rank, world = world_info(group)
+    k = host.shape[0]
+    sh = ColumnShards(k, world)
+    lo, hi = sh.range(rank)
+    mine = host[lo:hi].to(device, non_blocking=host.is_pinned())
+    return sh.gather_block(mine, group)

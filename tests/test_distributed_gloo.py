@@ -98,6 +98,24 @@ def _sharded_reduction_math(rank, world, port):
         dist.destroy_process_group()
 
 
+def _replicate(rank, world, port):
+    _init(rank, world, port)
+    from paper_1305_5120_b200.distributed import replicate_from_host
+    try:
+        for k, n in ((6, 4), (7, 3), (1, 5)):
+            host = torch.randn((k, n), dtype=torch.complex128,
+                               generator=torch.Generator().manual_seed(k + n))
+            got = replicate_from_host(host, torch.device("cpu"))
+            assert torch.equal(got, host)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_replicate_from_host_slabs():
+    """Each rank uploads one column slab; the all-gather rebuilds the whole matrix."""
+    mp.spawn(_replicate, args=(2, _free_port()), nprocs=2, join=True)
+
+
 def test_gloo_world2_sharded_reduction_decomposition():
     mp.spawn(_sharded_reduction_math, args=(2, _free_port()), nprocs=2, join=True)
 
@@ -238,3 +256,39 @@ def test_gloo_world2_sharded_generalized_matches_single(tmp_path):
     assert np.array_equal(g0["lam2"], g1["lam2"])
     assert np.max(np.abs(g0["lam2"] - lam2) / np.abs(lam2)) <= 1e-10
     assert O.largest_angle_sine(g0["c2"], c2.entries) < 1e-8
+
+
+def _sharded_public_filter(rank, world, port, out_dir):
+    _init(rank, world, port)
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    try:
+        torch.cuda.set_device(0)
+        h, lam, _ = baseline_matrix(6, 300)
+        y = _start_block(300, 21)
+        spec = G.FilterSpec(degree=11, a=float(lam[21]), b=float(lam[-1]) * 1.05,
+                            lam_ref=float(lam[0]))
+        G.reset_product_count()
+        out = G.chebyshev_filter(h, y, spec, group=dist.group.WORLD)
+        out2 = G.chebyshev_filter(G.HermitianDenseMatrix(h), G.VectorBlock(y), spec,
+                                  group=dist.group.WORLD)
+        np.savez(os.path.join(out_dir, f"f{rank}.npz"), out=out.entries, out2=out2.entries,
+                 count=G.product_count())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_world2_public_chebyshev_filter_group(tmp_path):
+    """chebyshev_filter(H, Y, spec, group=): host H replicated from per-rank slabs, Y
+    column-sharded, result gathered on every rank = the single-process filter."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    mp.spawn(_sharded_public_filter, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    f0, f1 = np.load(tmp_path / "f0.npz"), np.load(tmp_path / "f1.npz")
+    assert np.array_equal(f0["out"], f1["out"]) and int(f0["count"]) == 2 * 11 * 21
+    h, lam, _ = baseline_matrix(6, 300)
+    spec = G.FilterSpec(degree=11, a=float(lam[21]), b=float(lam[-1]) * 1.05, lam_ref=float(lam[0]))
+    ref = G.chebyshev_filter(h, _start_block(300, 21), spec).entries
+    assert np.linalg.norm(f0["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.linalg.norm(f0["out2"] - ref) <= 1e-12 * np.linalg.norm(ref)
