@@ -62,11 +62,14 @@ int chfsi_zgemm(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_
  *   2  op(B) = L^H, L lower (opb = C)           8  op(A) = L^H, L lower (opa = C)
  * The factor has order k; C holds its rows (flags 1, 8) or columns (2, 4)
  * [tri_offset, tri_offset + m or n): 0 for a whole factor, the shard start when a
- * rank computes a column range of L^-1 A L^-H (distributed.reduce_sharded). */
+ * rank computes a column range of L^-1 A L^-H (distributed.reduce_sharded).
+ * Flag 16 (combinable): C is Hermitian (m == n) and only the tiles touching its lower
+ * triangle are computed; the strictly upper part is left undefined. */
 #define CHFSI_TRI_A_LOWER 1
 #define CHFSI_TRI_B_UPPER 2
 #define CHFSI_TRI_B_LOWER 4
 #define CHFSI_TRI_A_UPPER 8
+#define CHFSI_TRI_C_LOWER 16
 int chfsi_zgemm_tri(chfsi_handle_t h, int opa, int opb, int64_t m, int64_t n, int64_t k,
                     double alpha_re, double alpha_im, const void* d_A, int64_t lda,
                     const void* d_B, int64_t ldb, double beta_re, double beta_im, void* d_C,

@@ -20,6 +20,8 @@ enum Tri : int {
   TRI_B_UPPER = 2,  // op(B) = L^H, L lower: column tile n0 needs k < n0 + BN
   TRI_B_LOWER = 4,  // B (op N) lower triangular: column tile n0 needs k >= n0
   TRI_A_UPPER = 8,  // op(A) = L^H, L lower: row tile m0 needs k >= m0
+  TRI_C_LOWER = 16, // C Hermitian (M == N): only tiles touching the lower triangle are
+                    // computed; the caller mirrors (mirror_lower) before using the upper
 };
 
 // D(8x8) += A(8x4, row) * B(4x8, col), all f64. One SASS DMMA.8x8x4.

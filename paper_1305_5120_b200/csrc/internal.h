@@ -147,6 +147,7 @@ int zdotc_cols(Handle* h, long long n, long long k, const double2* X, long long 
                const double2* Y, long long ldy, double2* out_dev);
 int hermitian_norms(Handle* h, long long n, const double2* A, long long lda, double* out2_dev);
 int hermitize(Handle* h, long long n, double2* A, long long lda);
+int mirror_lower(Handle* h, long long n, double2* A, long long lda);
 int clean_lower_factor(Handle* h, long long n, double2* L, long long ldl);
 int trtri_lower(Handle* h, long long n, const double2* L, long long ldl, double2* X, long long ldx);
 int zaxpby_cols(Handle* h, long long n, long long k, double2 alpha, const double2* X,

@@ -357,6 +357,40 @@ int hermitize(Handle* h, long long n, double2* A, long long lda) {
   return OK;
 }
 
+// Upper triangle <- conj(lower), real diagonal: completes a Hermitian matrix of which
+// only the lower triangle was computed (zgemm TRI_C_LOWER). Tile (r0, c0) above the
+// diagonal is filled from the transposed lower tile through shared memory.
+__global__ void mirror_lower_kernel(long long n, double2* A, long long lda) {
+  if (blockIdx.x < blockIdx.y) return;
+  __shared__ double2 lo[TS][TS + 1];
+  const long long r0 = (long long)blockIdx.y * TS, c0 = (long long)blockIdx.x * TS;
+  const int tx = threadIdx.x % TS, ty = threadIdx.x / TS;
+  for (int yy = ty; yy < TS; yy += 8) {
+    const long long r = c0 + tx, c = r0 + yy;  // lo[yy][tx] = A[c0 + tx, r0 + yy]
+    lo[yy][tx] = (r < n && c < n) ? A[r + c * lda] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int yy = ty; yy < TS; yy += 8) {
+    const long long r = r0 + tx, c = c0 + yy;  // A[r, c] = conj(A[c, r]) = conj(lo[tx][yy])
+    if (r >= n || c >= n) continue;
+    if (r < c) {
+      const double2 v = lo[tx][yy];
+      A[r + c * lda] = make_double2(v.x, -v.y);
+    } else if (r == c) {
+      A[r + c * lda].y = 0.0;
+    }
+  }
+}
+
+int mirror_lower(Handle* h, long long n, double2* A, long long lda) {
+  if (n <= 0) return OK;
+  const long long t = (n + TS - 1) / TS;
+  mirror_lower_kernel<<<dim3((unsigned)t, (unsigned)t), 256, 0, h->stream>>>(n, A, lda);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
 int clean_lower_factor(Handle* h, long long n, double2* L, long long ldl) {
   clean_lower_kernel<<<grid_for(n * n), 256, 0, h->stream>>>(n, L, ldl);
   h->launches++;

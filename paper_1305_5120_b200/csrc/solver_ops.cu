@@ -431,8 +431,10 @@ static int cholqr_pass_async(Handle* h, long long n, long long k, const double2*
   double2* G = (double2*)scratch(h, SLOT_SMALL, (size_t)k * k * sizeof(double2));
   double2* Li = (double2*)scratch(h, SLOT_SMALL2, (size_t)k * k * sizeof(double2));
   if (!G || !Li) return ERR_NOMEM;
-  CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, X, ldx, X, ldx, ZERO, G, k));
-  CHFSI_TRY(hermitize(h, k, G, k));
+  // Gram X^H X: lower-triangle tiles only (zpotrf reads the lower triangle; the mirror
+  // keeps G Hermitian for the shifted pass and for callers reading it whole)
+  CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, X, ldx, X, ldx, ZERO, G, k, TRI_C_LOWER));
+  CHFSI_TRY(mirror_lower(h, k, G, k));
   if (shift != 0.0) CHFSI_TRY(shift_diag(h, k, G, k, shift));
   int lwork = 0;
   CHFSI_SOLVER(cusolverDnZpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, (int)k,
@@ -444,7 +446,8 @@ static int cholqr_pass_async(Handle* h, long long n, long long k, const double2*
   h->launches++;
   CHFSI_TRY(get_real_diag(h, k, G, k, diag_dev));
   CHFSI_TRY(trtri_lower(h, k, G, k, Li, k));
-  CHFSI_TRY(zgemm(h, OP_N, OP_C, n, k, k, ONE, X, ldx, Li, k, ZERO, out, ldo));
+  // X R^-1 = X Li^H with Li = L^-1 lower triangular: skip its zero triangle
+  CHFSI_TRY(zgemm(h, OP_N, OP_C, n, k, k, ONE, X, ldx, Li, k, ZERO, out, ldo, TRI_B_UPPER));
   return OK;
 }
 

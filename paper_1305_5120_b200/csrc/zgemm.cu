@@ -474,7 +474,11 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
   // a triangular operand is square in the full factor; C covers rows (A flags) or
   // columns (B flags) [tri_off, tri_off + M or N) of it
   const bool a_tri = tri & (TRI_A_LOWER | TRI_A_UPPER), b_tri = tri & (TRI_B_LOWER | TRI_B_UPPER);
-  if (tri & ~(TRI_A_LOWER | TRI_B_UPPER | TRI_B_LOWER | TRI_A_UPPER)) {
+  if ((tri & TRI_C_LOWER) && M != N) {
+    set_error("zgemm: a lower-triangle-only C must be square");
+    return ERR_ARG;
+  }
+  if (tri & ~(TRI_A_LOWER | TRI_B_UPPER | TRI_B_LOWER | TRI_A_UPPER | TRI_C_LOWER)) {
     set_error("zgemm: unknown tri flags");
     return ERR_ARG;
   }

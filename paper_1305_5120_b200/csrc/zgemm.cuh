@@ -124,6 +124,7 @@ zgemm_dmma_kernel(const GemmParams p) {
   int mi, ni;
   tile_coords(p, blockIdx.x, mi, ni);
   const int m0 = mi * BM, n0 = ni * BN;
+  if ((p.tri & TRI_C_LOWER) && m0 + BM <= n0) return;  // strictly upper tile (CTA-uniform)
   int kbeg = 0, kend = p.K;
   if (EPI == EPI_PARTIAL) {
     kbeg = blockIdx.z * p.k_chunk;

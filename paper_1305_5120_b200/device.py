@@ -130,7 +130,7 @@ class Engine:
 
     # ------------------------------------------------------------ kernels
     # triangular-operand flags of chfsi_zgemm_tri (include/chfsi_b200.h)
-    TRI_A_LOWER, TRI_B_UPPER, TRI_B_LOWER, TRI_A_UPPER = 1, 2, 4, 8
+    TRI_A_LOWER, TRI_B_UPPER, TRI_B_LOWER, TRI_A_UPPER, TRI_C_LOWER = 1, 2, 4, 8, 16
 
     def zgemm(self, opa, opb, m, n, k, alpha, A, B, beta, C, tri=0, tri_offset=0):
         """C = alpha op(A) op(B) + beta C on column-major blocks (op: 'N' or 'C').

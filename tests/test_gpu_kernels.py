@@ -315,6 +315,28 @@ def test_triangle_skipping_gemm_and_reduction(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
+@pytest.mark.parametrize("cfg", [-1, 0, 1, 3, 5])
+@pytest.mark.parametrize("split", [0, 1, 4])
+def test_lower_only_gram(eng, cfg, split):
+    """TRI_C_LOWER: the Gram X^H X computes only tiles touching the lower triangle (the
+    CholQR Gram); its lower triangle equals the dense product."""
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    rng = np.random.default_rng(5 + cfg + split)
+    try:
+        assert lib.chfsi_gemm_override(cfg, split) == 0
+        for k, n in ((1, 50), (40, 700), (130, 2000), (257, 900)):
+            x = crand(rng, n, k)
+            g = D.zeros(k, k, eng.device)
+            eng.zgemm("C", "N", k, k, n, 1.0, D.to_device(x, eng.device),
+                      D.to_device(x, eng.device), 0.0, g, tri=eng.TRI_C_LOWER)
+            got = np.tril(D.to_host(g))
+            ref = np.tril(x.conj().T @ x)
+            assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref), k
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
 def test_trtri_blocked_matches_inverse(eng):
     """Recursive triangular inverse (its GEMMs skip the zero blocks of X11 / X22)."""
     from paper_1305_5120_b200 import device as D
