@@ -157,6 +157,14 @@ int chfsi_cholesky(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, int* h_i
 int chfsi_trtri_lower(chfsi_handle_t h, int64_t n, const void* d_L, int64_t ldl, void* d_X,
                       int64_t ldx);
 
+/* The replicated k x k step of a column-sharded CholQR pass (the multi-GPU form of
+ * core.py:365-382 `_qr_against_locked`, distributed.ShardedPhases): G <- (G + G^H)/2
+ * (+ shift I); *h_trace = trace(G); G = L L^H in place (zpotrf, lower); d_Li = L^-1;
+ * h_diag[k] = diag(L); *h_info = zpotrf info (0, or the 1-based failing pivot). */
+int chfsi_cholesky_inverse(chfsi_handle_t h, int64_t k, void* d_G, int64_t ldg, double shift,
+                           void* d_Li, int64_t ldli, double* h_diag, double* h_trace,
+                           int* h_info);
+
 /* core.py:172-188 `reduce_to_standard`: H = L^-1 A L^-H given d_Linv = L^-1 (lower
  * triangular with a zero upper triangle, e.g. from chfsi_trtri_lower). Two DMMA GEMMs
  * that skip the zero triangle of Linv; d_W is an n x n work block. H is not

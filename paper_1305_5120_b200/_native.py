@@ -66,6 +66,8 @@ SIGNATURES = {
     "chfsi_hermitian_norms": (_int, [_c_void_p, _i64, _c_void_p, _i64, _pdbl]),
     "chfsi_hermitize": (_int, [_c_void_p, _i64, _c_void_p, _i64]),
     "chfsi_cholesky": (_int, [_c_void_p, _i64, _c_void_p, _i64, _pint]),
+    "chfsi_cholesky_inverse": (_int, [_c_void_p, _i64, _c_void_p, _i64, _dbl, _c_void_p, _i64,
+                                       _pdbl, _pdbl, _pint]),
     "chfsi_reduce_to_standard": (_int, [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                          _c_void_p, _i64, _c_void_p, _i64]),
     "chfsi_trtri_lower": (_int, [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64]),

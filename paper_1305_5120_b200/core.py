@@ -476,6 +476,8 @@ class DeviceSolver:
         n = self.n
         for _ in range(dev.cols(f) + 2):
             try:
+                if self.sharded is not None:  # f is replicated and already projected
+                    return self.sharded.orthonormalize(self.eng, f, t, q, rank_tol=1e-14)
                 self.eng.orthonormalize(f, None if projected else locked, t, q, rank_tol=1e-14)
                 return q
             except RankDeficient as exc:
@@ -516,7 +518,11 @@ class DeviceSolver:
             # bootstrap: one unfiltered Rayleigh-Ritz pass on the start block
             t0 = time.perf_counter()
             q = self._orthonormalize(ws.z, None, ws.hq, ws.fa, rng)
-            w = self.eng.rayleigh_ritz(self.hb, q, ws.hq, ws.z, ws.hz)
+            if self.sharded is not None:
+                w, _, wvec = self.sharded.rayleigh_ritz(self.eng, self.hb, q, ws.hq, ws.fb, ws.hz)
+                self.sharded.ritz_columns(self.eng, q, wvec, 0, None, ws.z)
+            else:
+                w = self.eng.rayleigh_ritz(self.hb, q, ws.hq, ws.z, ws.hz)
             _count_products(s_tot)
             report.t_rr += time.perf_counter() - t0
             report.setup_matmuls += s_tot
@@ -551,9 +557,9 @@ class DeviceSolver:
             ev[2].record(self.eng.stream)
 
             if self.sharded is not None:
-                self.sharded.hq(self.eng, self.hb, q, ws.hq[:ncols])
-                w, res = self.eng.rayleigh_ritz_from_hq(q, ws.hq[:ncols], ws.z[:ncols],
-                                                        ws.hz[:ncols])
+                # f (in ws.fb) is dead after the QR: its buffer takes the own Ritz vectors
+                w, res, wvec = self.sharded.rayleigh_ritz(self.eng, self.hb, q, ws.hq[:ncols],
+                                                          ws.fb[:ncols], ws.hz[:ncols])
             else:
                 w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
                                                 ws.hz[:ncols], residuals=True)
@@ -569,7 +575,12 @@ class DeviceSolver:
             while kk < len(w) and res[kk] < cfg.tol and len(locked_vals) < nev:
                 locked_vals.append(float(w[kk]))
                 kk += 1
-            if kk:
+            if self.sharded is not None:
+                # newly locked vectors on every rank + this rank's next active shard
+                self.sharded.ritz_columns(self.eng, q, wvec, kk, ws.locked[nl:nl + kk],
+                                          ws.z[:ncols])
+                nl += kk
+            elif kk:
                 ws.locked[nl:nl + kk].copy_(ws.z[:kk])
                 nl += kk
             act = ws.z[kk:ncols]
@@ -609,9 +620,12 @@ class DeviceSolver:
 
         vals = np.asarray(locked_vals)
         t0 = time.perf_counter()
-        self.eng.zgemm("N", "N", n, nev, n, 1.0, self.hb, vecs, 0.0, ws.hq[:nev])
+        if self.sharded is not None:
+            final_res = self.sharded.residual_check(self.eng, self.hb, vecs, vals, ws.hq[:nev])
+        else:
+            self.eng.zgemm("N", "N", n, nev, n, 1.0, self.hb, vecs, 0.0, ws.hq[:nev])
+            final_res = self.eng.residual_norms(ws.hq[:nev], vecs, vals)
         _count_products(nev)
-        final_res = self.eng.residual_norms(ws.hq[:nev], vecs, vals)
         report.t_resid += time.perf_counter() - t0
         report.total_matmuls += nev
         report.t_total = time.perf_counter() - t_start

@@ -63,6 +63,9 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
                     double lam_ref, const double2* H_host, long long ldh_host, double2* H,
                     long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
                     int panels, int* result_in_w);
+int cholesky_inverse(Handle* h, long long k, double2* G, long long ldg, double shift,
+                     double2* Li, long long ldli, double* diag_host, double* trace_host,
+                     int* info_host);
 int reduce_to_standard(Handle* h, long long n, const double2* A, long long lda,
                        const double2* Linv, long long ldli, double2* W, long long ldw,
                        double2* H, long long ldh);
@@ -389,6 +392,18 @@ int chfsi_cholesky(chfsi_handle_t h, int64_t n, void* d_A, int64_t lda, int* h_i
   if (info != 0) return OK;  // caller maps info > 0 to NotPositiveDefinite(pivot)
   CHFSI_TRY(clean_lower_factor(h, n, (double2*)d_A, lda));
   return OK;
+}
+
+int chfsi_cholesky_inverse(chfsi_handle_t h, int64_t k, void* d_G, int64_t ldg, double shift,
+                           void* d_Li, int64_t ldli, double* h_diag, double* h_trace,
+                           int* h_info) {
+  H_CHECK(h);
+  if (k < 0 || ldg < k || ldli < k) {
+    set_error("cholesky_inverse: bad order or leading dimension");
+    return ERR_ARG;
+  }
+  return cholesky_inverse(h, k, (double2*)d_G, ldg, shift, (double2*)d_Li, ldli, h_diag,
+                          h_trace, h_info);
 }
 
 int chfsi_reduce_to_standard(chfsi_handle_t h, int64_t n, const void* d_A, int64_t lda,

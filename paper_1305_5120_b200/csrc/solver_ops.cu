@@ -528,6 +528,51 @@ int orthonormalize(Handle* h, long long n, long long k, double2* F, long long ld
   return OK;
 }
 
+// The replicated k x k step of a column-sharded CholQR pass (distributed.py
+// ShardedPhases.orthonormalize; the n-sized Gram and X R^-1 products are split over
+// the ranks by columns): G <- (G + G^H)/2 (+ shift I), trace(G) to the host, G = L L^H
+// (zpotrf, lower, in place), Li = L^-1, diag(L) and the zpotrf info to the host --
+// one host sync.
+int cholesky_inverse(Handle* h, long long k, double2* G, long long ldg, double shift,
+                     double2* Li, long long ldli, double* diag_host, double* trace_host,
+                     int* info_host) {
+  if (k <= 0) {
+    *info_host = 0;
+    *trace_host = 0.0;
+    return OK;
+  }
+  double* v = (double*)scratch(h, SLOT_VEC, (size_t)(2 * k + 2) * sizeof(double));
+  if (!v) return ERR_NOMEM;
+  double* dg = v;          // diag(G) before the factorisation
+  double* dl = v + k;      // diag(L)
+  int* info_dev = reinterpret_cast<int*>(v + 2 * k);
+  CHFSI_TRY(hermitize(h, k, G, ldg));
+  CHFSI_TRY(get_real_diag(h, k, G, ldg, dg));
+  if (shift != 0.0) CHFSI_TRY(shift_diag(h, k, G, ldg, shift));
+  int lwork = 0;
+  CHFSI_SOLVER(cusolverDnZpotrf_bufferSize(h->solver, CUBLAS_FILL_MODE_LOWER, (int)k,
+                                           (cuDoubleComplex*)G, (int)ldg, &lwork));
+  void* work = scratch(h, SLOT_SOLVER, (size_t)std::max(lwork, 1) * sizeof(cuDoubleComplex));
+  if (!work) return ERR_NOMEM;
+  CHFSI_CUDA(cudaMemsetAsync(info_dev, 0, sizeof(int), h->stream));
+  CHFSI_SOLVER(cusolverDnZpotrf(h->solver, CUBLAS_FILL_MODE_LOWER, (int)k, (cuDoubleComplex*)G,
+                                (int)ldg, (cuDoubleComplex*)work, lwork, info_dev));
+  h->launches++;
+  CHFSI_TRY(get_real_diag(h, k, G, ldg, dl));
+  CHFSI_TRY(trtri_lower(h, k, G, ldg, Li, ldli));
+  const size_t bytes = (size_t)(2 * k) * sizeof(double) + sizeof(int);
+  double* hb = pinned(h, bytes + 16);
+  if (!hb) return ERR_NOMEM;
+  CHFSI_CUDA(cudaMemcpyAsync(hb, v, bytes, cudaMemcpyDeviceToHost, h->stream));
+  CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  double tr = 0.0;
+  for (long long j = 0; j < k; ++j) tr += hb[j];
+  *trace_host = tr;
+  std::copy(hb + k, hb + 2 * k, diag_host);
+  *info_host = *reinterpret_cast<int*>(hb + 2 * k);
+  return OK;
+}
+
 // CGS2 projection of F against the locked block L (first half of core.py:371-372);
 // column-local, so a column-sharded caller can run it on its own shard only.
 int project_out(Handle* h, long long n, long long k, double2* F, long long ldf,

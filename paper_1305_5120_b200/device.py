@@ -268,6 +268,18 @@ class Engine:
             raise ContractViolation(f"zpotrf: illegal argument {-info.value}")
         return A
 
+    def cholesky_inverse(self, G, Li, shift=0.0):
+        """Symmetrise G (+ shift I), factor G = L L^H in place and write Li = L^-1
+        (chfsi_cholesky_inverse). Returns (diag(L), trace(G), zpotrf info)."""
+        k = rows(G)
+        diag = np.empty(k, dtype=np.float64)
+        tr = ctypes.c_double(0.0)
+        info = ctypes.c_int(0)
+        _native.call("chfsi_cholesky_inverse", self.h, k, ptr(G), ld(G), float(shift), ptr(Li),
+                     ld(Li), diag.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                     ctypes.byref(tr), ctypes.byref(info))
+        return diag, float(tr.value), int(info.value)
+
     def reduce_to_standard(self, A, Linv, W, H):
         """H = Linv A Linv^H (chfsi_reduce_to_standard); W is an n x n work block."""
         n = rows(A)

@@ -121,29 +121,41 @@ def all_gather_values(vals, shards, group=None):
 class ShardedPhases:
     """Column-sharded phases of one outer iteration.
 
-    * ``filter_project``: each rank filters its contiguous column range of the
-      active block (core.py:276-283 is column-separable) and projects it
-      against the locked block (CGS2 is column-local too), then the shards are
-      all-gathered: every rank holds the full projected block.
-    * ``hq``: H Q_p on own columns, all-gathered into HQ (the n^2 k term of
-      Rayleigh-Ritz).
-    CholQR2, the k x k eigenproblem, Z = QW, HZ = HQ W and the residuals run
-    redundantly on identical inputs with deterministic kernels, so every rank
-    reaches the same Ritz values and locking decision with no further
-    collective. The only collectives are two all-gathers per iteration.
+    Every n-sized product is split over the ranks by columns and followed by an
+    all-gather of the column shards (NCCL over NVLink); only k x k work (Cholesky
+    factors, the k x k eigenproblem) and the locking decision are replicated, on
+    identical gathered inputs with deterministic kernels, so every rank reaches the
+    same Ritz values and locking decision.
+
+    * ``filter_project``: each rank filters its contiguous column range of the active
+      block (core.py:276-283 is column-separable) and projects it against the locked
+      block (CGS2 is column-local too); gather F.
+    * ``orthonormalize``: CholQR2 (shifted CholQR3 fallback) with the Gram X^H X[:, p]
+      and X R^-1[:, p] of each pass computed per column shard; gather G, gather Q.
+    * ``rayleigh_ritz``: H Q[:, p] (gather HQ), Q^H HQ[:, p] (gather G), replicated
+      zheevd, then Z[:, p] = Q W[:, p], HZ[:, p] = HQ W[:, p] and the residual norms of
+      the own columns (gather k doubles).
+    * ``ritz_columns``: after locking each rank forms only the Ritz vectors it needs
+      next -- the newly locked ones (replicated) and its shard of the new active
+      block -- straight from the replicated Q and W, so re-sharding costs no
+      communication.
     """
 
     def __init__(self, group=None):
         self.group = group
         self.rank, self.world = world_info(group)
-        self._buf = None
+        self._bufs = {}
+
+    def _scratch(self, name, k, n, like):
+        buf = self._bufs.get(name)
+        if buf is None or buf.shape[0] < k or buf.shape[1] != n or buf.device != like.device:
+            buf = torch.empty((k, n), dtype=like.dtype, device=like.device)
+            self._bufs[name] = buf
+        return buf[:k]
 
     def _gather(self, sh, mine, out):
         n = out.shape[1]
-        need = sh.padded * self.world
-        if self._buf is None or self._buf.shape[0] < need or self._buf.shape[1] != n:
-            self._buf = torch.empty((need, n), dtype=out.dtype, device=out.device)
-        gathered = self._buf[:need]
+        gathered = self._scratch(("gather", n), sh.padded * self.world, n, out)
         sh.all_gather(mine, gathered, self.group)
         return sh.compact(gathered, out)
 
@@ -158,13 +170,121 @@ class ShardedPhases:
             mine = active[lo:hi]
         return self._gather(sh, mine, other[:k])
 
-    def hq(self, eng, H, Q, HQ):
-        k, n = Q.shape[0], Q.shape[1]
+    def orthonormalize(self, eng, F, T, Q, rank_tol=1e-14):
+        """CholQR2 of the replicated block F (already projected against the locked
+        block) into Q, T a work block; same rank test and shifted-CholQR3 fallback as
+        csrc/solver_ops.cu `orthonormalize` (core.py:365-382). Raises
+        RankDeficient(column)."""
+        import numpy as np
+
+        from .errors import RankDeficient
+        k, n = F.shape
+        sh = ColumnShards(k, self.world)
+        lo, hi = sh.range(self.rank)
+        w = hi - lo
+        G = self._scratch("g", k, k, F)
+        Li = self._scratch("li", k, k, F)
+
+        def gram(X):  # G[:, p] = X^H X[:, p], gathered
+            if w:
+                eng.zgemm("C", "N", k, w, n, 1.0, X, X[lo:hi], 0.0, G[lo:hi])
+            self._gather(sh, G[lo:hi], G)
+
+        def apply(X, out):  # out[:, p] = X Li^H[:, p] (Li^H upper: skip its zeros)
+            if w:
+                eng.zgemm("N", "C", n, w, k, 1.0, X, Li[:, lo:hi], 0.0, out[lo:hi],
+                          tri=eng.TRI_B_UPPER, tri_offset=lo)
+            self._gather(sh, out[lo:hi], out)
+
+        gram(F)
+        d1, tr, info1 = eng.cholesky_inverse(G, Li)
+        fro = float(np.sqrt(max(tr, 0.0)))
+        if info1 != 0:
+            # first Cholesky broke down: shifted CholQR3 (Fukaya et al.),
+            # s = 11 (n k + k (k+1)) u ||F||_F^2, then two plain passes
+            u = 1.1102230246251565e-16
+            shift = 11.0 * (n * k + k * (k + 1)) * u * fro * fro
+            gram(F)
+            d1, _, info1 = eng.cholesky_inverse(G, Li, shift)
+            apply(F, T)
+            gram(T)
+            d2, _, info2 = eng.cholesky_inverse(G, Li)
+            apply(T, Q)
+            gram(Q)
+            d3, _, info3 = eng.cholesky_inverse(G, Li)
+            apply(Q, T)
+            Q.copy_(T)
+            infos, diags = (info1, info2, info3), (d1, d2, d3)
+        else:
+            apply(F, T)
+            gram(T)
+            d2, _, info2 = eng.cholesky_inverse(G, Li)
+            apply(T, Q)
+            infos, diags = (info1, info2), (d1, d2)
+        for info in infos:
+            if info != 0:
+                raise RankDeficient(int(info) - 1)
+        r = np.abs(np.prod(np.stack(diags), axis=0))
+        bad = np.nonzero(r < rank_tol * fro)[0]
+        if bad.size:
+            raise RankDeficient(int(bad[0]))
+        return Q
+
+    def rayleigh_ritz(self, eng, H, Q, HQ, Z, HZ):
+        """core.py:318-330 + the residuals of core.py:477, column-sharded: returns the
+        Ritz values, all residual norms (gathered) and the eigenvector block W (k x k,
+        replicated). Z and HZ receive the own columns only."""
+        import numpy as np
+        k, n = Q.shape
+        sh = ColumnShards(k, self.world)
+        lo, hi = sh.range(self.rank)
+        w_ = hi - lo
+        if w_:
+            eng.zgemm("N", "N", n, w_, n, 1.0, H, Q[lo:hi], 0.0, HQ[lo:hi])
+        self._gather(sh, HQ[lo:hi], HQ)
+        W = self._scratch("w", k, k, Q)
+        if w_:
+            eng.zgemm("C", "N", k, w_, n, 1.0, Q, HQ[lo:hi], 0.0, W[lo:hi])
+        self._gather(sh, W[lo:hi], W)
+        eng.hermitize(W)
+        lam = eng.heevd(W)  # W <- eigenvectors, ascending
+        if w_:
+            eng.zgemm("N", "N", n, w_, k, 1.0, Q, W[lo:hi], 0.0, Z[lo:hi])
+            eng.zgemm("N", "N", n, w_, k, 1.0, HQ, W[lo:hi], 0.0, HZ[lo:hi])
+            mine = eng.residual_norms(HZ[lo:hi], Z[lo:hi], lam[lo:hi])
+        else:
+            mine = np.empty(0)
+        res = all_gather_values(torch.from_numpy(np.ascontiguousarray(mine)).to(Q.device), sh,
+                                self.group)
+        return lam, res.cpu().numpy(), W
+
+    def ritz_columns(self, eng, Q, W, kk, locked_out, z):
+        """After locking kk leading Ritz pairs: the newly locked vectors Q W[:, :kk] on
+        every rank, and this rank's shard of the new active block Q W[:, kk:] into
+        z[kk + lo : kk + hi] (the shard the next filter_project will read)."""
+        k, n = Q.shape
+        if kk:
+            eng.zgemm("N", "N", n, kk, k, 1.0, Q, W[:kk], 0.0, locked_out)
+        sh = ColumnShards(k - kk, self.world)
+        lo, hi = sh.range(self.rank)
+        if hi > lo:
+            eng.zgemm("N", "N", n, hi - lo, k, 1.0, Q, W[kk + lo:kk + hi], 0.0,
+                      z[kk + lo:kk + hi])
+
+    def residual_check(self, eng, H, V, vals, HV):
+        """Final re-check ||H v_j - lambda_j v_j|| (core.py:532-544), column-sharded."""
+        import numpy as np
+        k, n = V.shape
         sh = ColumnShards(k, self.world)
         lo, hi = sh.range(self.rank)
         if hi > lo:
-            eng.zgemm("N", "N", n, hi - lo, n, 1.0, H, Q[lo:hi], 0.0, HQ[lo:hi])
-        return self._gather(sh, HQ[lo:hi], HQ[:k])
+            eng.zgemm("N", "N", n, hi - lo, n, 1.0, H, V[lo:hi], 0.0, HV[lo:hi])
+            mine = eng.residual_norms(HV[lo:hi], V[lo:hi], vals[lo:hi])
+        else:
+            mine = np.empty(0)
+        res = all_gather_values(torch.from_numpy(np.ascontiguousarray(mine)).to(V.device), sh,
+                                self.group)
+        return res.cpu().numpy()
 
 
 def reduction_bounds(n, world, align=64):

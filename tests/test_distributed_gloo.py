@@ -292,3 +292,73 @@ def test_gloo_world2_public_chebyshev_filter_group(tmp_path):
     ref = G.chebyshev_filter(h, _start_block(300, 21), spec).entries
     assert np.linalg.norm(f0["out"] - ref) <= 1e-12 * np.linalg.norm(ref)
     assert np.linalg.norm(f0["out2"] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def _sharded_orth(rank, world, port, out_dir):
+    _init(rank, world, port)
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.distributed import ShardedPhases
+    from paper_1305_5120_b200.errors import RankDeficient
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        eng = D.Engine.get(dev)
+        ph = ShardedPhases(dist.group.WORLD)
+        out = {}
+        for name, f in _orth_cases().items():
+            n, k = f.shape
+            F = D.to_device(f, dev)
+            T, Q = D.empty(n, k, dev), D.empty(n, k, dev)
+            try:
+                ph.orthonormalize(eng, F, T, Q)
+                out[name] = D.to_host(Q)
+            except RankDeficient as exc:
+                out[name + "_bad"] = np.array([exc.column])
+        np.savez(os.path.join(out_dir, f"o{rank}.npz"), **out)
+    finally:
+        dist.destroy_process_group()
+
+
+def _orth_cases():
+    rng = np.random.default_rng(44)
+    n, k = 600, 37
+    good = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    # ill-conditioned (cond ~ 1e10): the first Cholesky breaks down -> shifted CholQR3
+    u, _ = np.linalg.qr(good)
+    ill = u @ np.diag(np.logspace(0, -10, k)) @ np.linalg.qr(rng.standard_normal((k, k)))[0]
+    dup = good.copy()
+    dup[:, 20] = dup[:, 3]
+    return {"good": good, "ill": ill, "dup": dup}
+
+
+@pytest.mark.gpu
+def test_gloo_world2_sharded_cholqr_matches_fused(tmp_path):
+    """ShardedPhases.orthonormalize (per-column-shard Gram and X R^-1, gathered) gives
+    an orthonormal basis of the same subspace as the fused single-GPU CholQR2, takes
+    the shifted CholQR3 path on an ill-conditioned block and reports the same
+    rank-collapse column."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.errors import RankDeficient
+    mp.spawn(_sharded_orth, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    o0, o1 = np.load(tmp_path / "o0.npz"), np.load(tmp_path / "o1.npz")
+    eng = D.Engine.get(torch.device("cuda", 0))
+    for name, f in _orth_cases().items():
+        n, k = f.shape
+        try:
+            eng.orthonormalize(D.to_device(f, eng.device), None, D.empty(n, k, eng.device),
+                               q := D.empty(n, k, eng.device))
+            ref, bad = D.to_host(q), None
+        except RankDeficient as exc:
+            ref, bad = None, exc.column
+        if bad is not None:
+            assert int(o0[name + "_bad"][0]) == bad == int(o1[name + "_bad"][0]), name
+            continue
+        got = o0[name]
+        assert np.array_equal(got, o1[name])
+        assert np.linalg.norm(got.conj().T @ got - np.eye(k)) <= 1e-12, name
+        # the block lies in range(Q); for the well-conditioned block the subspace equals
+        # the fused CholQR2's (an ill-conditioned block fixes its range only to u cond)
+        assert np.linalg.norm(f - got @ (got.conj().T @ f)) <= 1e-12 * np.linalg.norm(f), name
+        if name == "good":
+            assert O.largest_angle_sine(got, ref) < 1e-8, name
