@@ -137,6 +137,10 @@ def main():
         entry = {"problem": ell, "s_per_solve": dt, "outer_iterations": rep.outer_iterations,
                  "total_matmuls": rep.total_matmuls, "t_filter": rep.t_filter, "t_qr": rep.t_qr,
                  "t_rr": rep.t_rr, "filter_tflops": rep.filter_tflops,
+                 "t_lanczos": rep.t_lanczos, "t_resid": rep.t_resid,
+                 # per-iteration phase times (the input of scripts/scaling_model.py)
+                 "iterations": [[i.filtered_cols, i.converged, i.t_filter, i.t_qr, i.t_rr]
+                                for i in rep.iterations],
                  "max_residual": float(np.max(res)), "orthonormality": orth,
                  "lam_first": float(lamc[0]), "lam_last": float(lamc[-1])}
         if ell == 1 and smat is None:
