@@ -337,6 +337,30 @@ def test_lower_only_gram(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
+def test_cholesky_inverse_step(eng):
+    """chfsi_cholesky_inverse (replicated k x k step of a sharded CholQR pass):
+    symmetrise, shift, factor, invert; diag(L), trace and the zpotrf pivot."""
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(21)
+    for k in (1, 33, 300):
+        x = crand(rng, 4 * k, k)
+        g = x.conj().T @ x
+        g_asym = g + 1e-13 * np.linalg.norm(g) * crand(rng, k, k)  # gathered, not Hermitian
+        dG, dLi = D.to_device(g_asym, eng.device), D.empty(k, k, eng.device)
+        diag, tr, info = eng.cholesky_inverse(dG, dLi, shift=0.5)
+        gh = (g_asym + g_asym.conj().T) / 2 + 0.5 * np.eye(k)
+        lo = np.linalg.cholesky(gh)
+        assert info == 0
+        assert abs(tr - np.trace(g_asym).real) <= 1e-12 * abs(tr)
+        assert np.allclose(diag, np.diag(lo).real, rtol=1e-12, atol=0)
+        li = D.to_host(dLi)
+        assert np.array_equal(np.triu(li, 1), np.zeros((k, k)))
+        assert np.linalg.norm(li @ lo - np.eye(k)) <= 1e-11 * k
+    bad = np.diag([4.0, 1.0, -1.0, 2.0]).astype(complex)
+    _, _, info = eng.cholesky_inverse(D.to_device(bad, eng.device), D.empty(4, 4, eng.device))
+    assert info == 3
+
+
 def test_trtri_blocked_matches_inverse(eng):
     """Recursive triangular inverse (its GEMMs skip the zero blocks of X11 / X22)."""
     from paper_1305_5120_b200 import device as D
