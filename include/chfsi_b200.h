@@ -188,6 +188,14 @@ int chfsi_gemm_override(int cfg, int split);
 int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m,
                     int64_t n, int64_t k, int* h_cfg, int* h_split);
 
+/* Complex-product scheme of the op N x N (TMA) GEMMs, process-wide: 3 = 3M (three real
+ * DMMA products per complex multiply-add: Ar Br, Ai Bi, (Ar+Ai)(Br+Bi); default) or
+ * 4 = four real products. Replaces the inner kernel of linalg.py:198-251 `gemm`
+ * (numpy/OpenBLAS zgemm). Environment CHFSI_COMPLEX_MUL=4 selects 4 at load time.
+ * chfsi_get_complex_mul returns the current scheme. */
+int chfsi_set_complex_mul(int mul);
+int chfsi_get_complex_mul(void);
+
 /* Microbenchmarks that give the roofline denominators on the box:
  * FP64 tensor-pipe (DMMA) and FP64 FMA-pipe (DFMA) peak, TFLOP/s. */
 int chfsi_peak_dmma(int device, int iters, double* h_tflops);

@@ -444,6 +444,10 @@ int chfsi_axpby(chfsi_handle_t h, int64_t n, int64_t k, double alpha_re, double 
 
 int chfsi_gemm_override(int cfg, int split) { return gemm_override(cfg, split); }
 
+int chfsi_set_complex_mul(int mul) { return set_complex_mul(mul); }
+
+int chfsi_get_complex_mul(void) { return complex_mul(); }
+
 int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m, int64_t n,
                     int64_t k, int* h_cfg, int* h_split) {
   H_CHECK(h);

@@ -133,6 +133,8 @@ size_t filter_step_workspace(Handle* h, long long M, long long N);
 // Tuning hooks: force a tile config (-1 = cost model) / split-K factor (0 = auto).
 int gemm_override(int cfg, int split);
 void gemm_overrides(int* cfg, int* split);
+int set_complex_mul(int mul);
+int complex_mul();
 int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
               int* cfg, int* split);
 

@@ -85,8 +85,9 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 11;
+constexpr int NCFG = 14;
 constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
+constexpr int FIRST_3M = 11;  // cfgs >= 11: the TMA kernels with 3M complex products
 // cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
 // cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
 // cfg 2: 64x16   BK8  warp 16x16 (4 warps)     cfg 6: 128x32 BK8  warp 32x16 (8 warps)
@@ -102,12 +103,12 @@ using C6 = CfgT<128, 32, 8, 32, 16, 4>;
 // cfg 10: TMA 64x32 with four 16x32 warps stacked by rows (same fragment loads per DMMA as
 // cfg 7; on a ragged column edge every warp keeps the same number of live 8-column blocks)
 using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmParams);
-template <int BM, int BN, int WM, int WN, int ST, int MINB = 1>
+template <int BM, int BN, int WM, int WN, int ST, int MINB = 1, int MUL = 4>
 struct TmaT {
   static constexpr int threads = (BM / WM) * (BN / WN) * 32;
   static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST>(); }
   template <int EPI>
-  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB>; }
+  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB, MUL>; }
 };
 // (explicit min-blocks keep ptxas at <= 128 regs -> 4 CTAs / SM for the 64x32 tile;
 // a register-double-buffered fragment variant measured 1.5-2 % slower, profiles/r01)
@@ -115,11 +116,22 @@ using T7 = TmaT<64, 32, 32, 16, 4, 4>;
 using T8 = TmaT<64, 16, 16, 16, 4, 4>;
 using T9 = TmaT<64, 64, 32, 32, 4, 2>;
 using T10 = TmaT<64, 32, 16, 32, 4, 4>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8};
-const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32};  // warp tile width
+// cfg 11 / 12: cfg 7 / cfg 10 with 3M complex products (three real DMMA products per
+// complex MAC; 48 accumulator doubles per thread -> 3 CTAs / SM)
+using T11 = TmaT<64, 32, 32, 16, 4, 3, 3>;
+using T12 = TmaT<64, 32, 16, 32, 4, 3, 3>;
+// cfg 13: 3M, 64x32 with eight 16x16 warps (24 accumulator doubles: 2 CTAs / SM = 16 warps)
+using T13 = TmaT<64, 32, 16, 16, 4, 2, 3>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8};
+const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16};  // warp tile width
 bool g_tma_enabled = true;
+// complex products in the TMA kernels: 3 (3M, default) or 4 real DMMA products
+int g_mul = [] {
+  const char* e = getenv("CHFSI_COMPLEX_MUL");
+  return (e && atoi(e) == 4) ? 4 : 3;
+}();
 int g_force_cfg = -1, g_force_split = 0;
 
 struct Entry {
@@ -173,6 +185,9 @@ int ensure_table() {
   put_tma<T8>(8);
   put_tma<T9>(9);
   put_tma<T10>(10);
+  put_tma<T11>(11);
+  put_tma<T12>(12);
+  put_tma<T13>(13);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -215,7 +230,7 @@ struct Plan {
 //     warps (ncu: DMMA pipe 92.5 % vs 95.7 % active at k = 210): x (1 + kRag / tiles_n);
 //   * split-K adds the reduce pass: kTred + (s + 3) M N 16 B at HBM speed.
 constexpr double kEffNN[NCFG] = {0.906, 0.898, 0.837, 0.823, 0.911, 0.926, 0.885,
-                                 0.966, 0.915, 0.962, 0.954};
+                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13};
 constexpr double kEffCN[7] = {0.886, 0.927, 0.877, 0.854, 1.058, 0.971, 0.887};
 constexpr double kR0Warps4 = 1.289, kR0Warps8 = 1.108;
 constexpr double kRag = 0.122, kFloor = 0.859;
@@ -262,6 +277,7 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
     if (c >= FIRST_TMA && !g_tma_enabled) continue;
+    if (g_force_cfg < 0 && c >= FIRST_TMA && (c >= FIRST_3M) != (g_mul == 3)) continue;
     const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
     if (!e.ready && !ep.ready) continue;
@@ -293,10 +309,11 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
 // per-call host cost of a small GEMM is a hash lookup (the solve's tail issues
 // thousands of identical small products).
 struct PlanKey {
-  int opa, opb, epi, fcfg, fsplit;
+  int opa, opb, epi, fcfg, fsplit, mul;
   long long M, N, K;
   bool operator==(const PlanKey& o) const {
     return opa == o.opa && opb == o.opb && epi == o.epi && fcfg == o.fcfg && fsplit == o.fsplit &&
+           mul == o.mul &&
            M == o.M && N == o.N && K == o.K;
   }
 };
@@ -312,7 +329,7 @@ struct PlanKeyHash {
 
 Plan cached_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
   static std::unordered_map<PlanKey, Plan, PlanKeyHash> cache;
-  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, M, N, K};
+  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, g_mul, M, N, K};
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   const Plan pl = choose(h, opa, opb, epi, M, N, K);
@@ -443,6 +460,17 @@ int gemm_override(int cfg, int split) {
   g_force_split = split;
   return OK;
 }
+
+int set_complex_mul(int mul) {
+  if (mul != 3 && mul != 4) {
+    set_error("set_complex_mul: mul must be 3 (3M) or 4");
+    return ERR_ARG;
+  }
+  g_mul = mul;
+  return OK;
+}
+
+int complex_mul() { return g_mul; }
 
 void gemm_overrides(int* cfg, int* split) {
   *cfg = g_force_cfg;

@@ -74,6 +74,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ double2 lds128(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); }
 
 // Stage refill lag: at k-tile kt the producer lane refills the stage of tile
@@ -83,12 +89,107 @@ __device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); 
 #endif
 constexpr int kDefer = CHFSI_TMA_DEFER;
 
+// One k-tile sweep per stage: wait for the stage, run the BK/4 DMMA k-steps of the
+// warp tile, release the stage, and (rotating producer lane) refill the stage that
+// was released one iteration earlier.
+template <int BM, int BN, int WM, int WN, int STAGES, int MUL, bool RAGGED, class Issue>
+__device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2* sA,
+                                             const double2* sB, uint64_t* full, uint64_t* empty,
+                                             Issue& issue, int KT, int wm, int wn, int lane,
+                                             int warp, int fc, int pr, int jvalid,
+                                             double (&c0)[WM / 8][WN / 8][2],
+                                             double (&c1)[WM / 8][WN / 8][2],
+                                             double (&c2)[WM / 8][WN / 8][2]) {
+  constexpr int BK = 8;
+  constexpr int NWARP = (BM / WM) * (BN / WN);
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
+  (void)p;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    const unsigned phase = (kt / STAGES) & 1;
+    mbar_wait(&full[s], phase);
+    // 32-bit shared-window addresses: LDS instead of generic loads (fewer address
+    // registers, shorter load-to-use latency)
+    const unsigned a = smem_u32(sA + s * A_ELEMS);
+    const unsigned b = smem_u32(sB + s * B_ELEMS);
+    #pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int kk = ks * 4 + fc;
+      double2 fa[FM], fb[FN];
+      #pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        const int mg = (wm * WM) / 8 + i;
+        fa[i] = lds128(a + 16u * ((mg * BK + kk) * 8 + (pr ^ kk)));
+      }
+      #pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const int nn = wn * WN + j * 8 + pr;
+        fb[j] = lds128(b + 16u * (nn * 8 + (kk ^ pr)));
+      }
+      if (MUL == 3) {
+        // 3M: three real products per complex MAC. The operand sums cost FM + FN DADDs
+        // per 3 FM FN DMMAs.
+        double as[FM], bs[FN];
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) as[i] = fa[i].x + fa[i].y;
+        #pragma unroll
+        for (int j = 0; j < FN; ++j) bs[j] = fb[j].x + fb[j].y;
+        #pragma unroll
+        for (int i = 0; i < FM; ++i)
+          #pragma unroll
+          for (int j = 0; j < FN; ++j)
+            if (!RAGGED || j < jvalid) {
+              dmma884(c0[i][j][0], c0[i][j][1], fa[i].x, fb[j].x);
+              dmma884(c1[i][j][0], c1[i][j][1], fa[i].y, fb[j].y);
+            }
+        #pragma unroll
+        for (int i = 0; i < FM; ++i)
+          #pragma unroll
+          for (int j = 0; j < FN; ++j)
+            if (!RAGGED || j < jvalid) dmma884(c2[i][j][0], c2[i][j][1], as[i], bs[j]);
+      } else {
+        // two sweeps over the warp tile: the second update of each accumulator is
+        // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
+        #pragma unroll
+        for (int i = 0; i < FM; ++i)
+          #pragma unroll
+          for (int j = 0; j < FN; ++j)
+            if (!RAGGED || j < jvalid) {
+              dmma884(c0[i][j][0], c0[i][j][1], fa[i].x, fb[j].x);
+              dmma884(c1[i][j][0], c1[i][j][1], fa[i].x, fb[j].y);
+            }
+        #pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const double nai = -fa[i].y;
+          #pragma unroll
+          for (int j = 0; j < FN; ++j)
+            if (!RAGGED || j < jvalid) {
+              dmma884(c0[i][j][0], c0[i][j][1], nai, fb[j].y);
+              dmma884(c1[i][j][0], c1[i][j][1], fa[i].y, fb[j].x);
+            }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill the stage released one iteration ago with tile kt - 1 + STAGES: by now
+    // every warp has normally finished tile kt - 1, so this empty-barrier wait is
+    // almost always already complete and the producer lane does not stall its warp
+    // (waiting on the just-released stage cost ~8 % of warp samples, profiles/r01)
+    if (lane == 0 && kt >= kDefer && warp == (kt % NWARP) && kt - kDefer + STAGES < KT) {
+      mbar_wait(&empty[(kt - kDefer) % STAGES], ((kt - kDefer) / STAGES) & 1);
+      issue(kt - kDefer + STAGES);
+    }
+  }
+}
+
 template <int BM, int BN, int WM, int WN, int STAGES>
 constexpr int zgemm_tma_smem_bytes() {
   return STAGES * (BM * 8 + BN * 8) * 16 + 1024 /* alignment slack */ + 2 * STAGES * 8;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1>
+template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1, int MUL = 4>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const GemmParams p) {
@@ -152,133 +253,30 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       if (s < KT) issue(s);
   }
 
-  double cr[FM][FN][2], ci[FM][FN][2];
-  #pragma unroll
-  for (int i = 0; i < FM; ++i)
-    #pragma unroll
-    for (int j = 0; j < FN; ++j) {
-      cr[i][j][0] = cr[i][j][1] = 0.0;
-      ci[i][j][0] = ci[i][j][1] = 0.0;
-    }
-
   const int fr = lane >> 2, fc = lane & 3;
   const int pr = perm8(fr);
+  (void)fr;
   // 8-column MMA blocks of this warp that hold at least one real column: blocks
   // entirely past N (the padded tail of a narrow filter block) issue no DMMAs.
   // Warp-uniform, so DMMA's warp-collective semantics are kept.
   const int jvalid = min(FN, max(0, (p.N - (n0 + wn * WN) + 7) / 8));
+  // MUL == 4: c0 = Re, c1 = Im, four real products per complex MAC.
+  // MUL == 3: c0 = Ar Br, c1 = Ai Bi, c2 = (Ar + Ai)(Br + Bi) (3M); the epilogue forms
+  // Re = c0 - c1, Im = c2 - c0 - c1.
+  double c0[FM][FN][2], c1[FM][FN][2], c2[FM][FN][2];
+  #pragma unroll
+  for (int i = 0; i < FM; ++i)
+    #pragma unroll
+    for (int j = 0; j < FN; ++j)
+      #pragma unroll
+      for (int t = 0; t < 2; ++t) c0[i][j][t] = c1[i][j][t] = c2[i][j][t] = 0.0;
+
   if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      const unsigned phase = (kt / STAGES) & 1;
-      mbar_wait(&full[s], phase);
-      const double2* a = sA + s * A_ELEMS;
-      const double2* b = sB + s * B_ELEMS;
-      #pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        const int kk = ks * 4 + fc;
-        double2 fa[FM], fb[FN];
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int mg = (wm * WM) / 8 + i;
-          fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
-        }
-        #pragma unroll
-        for (int j = 0; j < FN; ++j) {
-          const int nn = wn * WN + j * 8 + pr;
-          fb[j] = b[nn * 8 + (kk ^ pr)];
-        }
-        // two sweeps over the warp tile: the second update of each accumulator is
-        // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          #pragma unroll
-          for (int j = 0; j < FN; ++j) {
-            {
-              dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
-              dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
-            }
-          }
-        }
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const double nai = -fa[i].y;
-          #pragma unroll
-          for (int j = 0; j < FN; ++j) {
-            {
-              dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
-              dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the stage released one iteration ago with tile kt - 1 + STAGES: by now
-      // every warp has normally finished tile kt - 1, so this empty-barrier wait is
-      // almost always already complete and the producer lane does not stall its warp
-      // (waiting on the just-released stage cost ~8 % of warp samples, profiles/r01)
-      if (lane == 0 && kt >= kDefer && warp == (kt % NWARP) && kt - kDefer + STAGES < KT) {
-        mbar_wait(&empty[(kt - kDefer) % STAGES], ((kt - kDefer) / STAGES) & 1);
-        issue(kt - kDefer + STAGES);
-      }
-    }
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, false>(p, sA, sB, full, empty, issue, KT, wm, wn,
+                                                    lane, warp, fc, pr, jvalid, c0, c1, c2);
   } else {  // ragged column edge: skip 8-column blocks past N
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      const unsigned phase = (kt / STAGES) & 1;
-      mbar_wait(&full[s], phase);
-      const double2* a = sA + s * A_ELEMS;
-      const double2* b = sB + s * B_ELEMS;
-      #pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        const int kk = ks * 4 + fc;
-        double2 fa[FM], fb[FN];
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int mg = (wm * WM) / 8 + i;
-          fa[i] = a[(mg * BK + kk) * 8 + (pr ^ kk)];
-        }
-        #pragma unroll
-        for (int j = 0; j < FN; ++j) {
-          const int nn = wn * WN + j * 8 + pr;
-          fb[j] = b[nn * 8 + (kk ^ pr)];
-        }
-        // two sweeps over the warp tile: the second update of each accumulator is
-        // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          #pragma unroll
-          for (int j = 0; j < FN; ++j) {
-            if (j < jvalid) {
-              dmma884(cr[i][j][0], cr[i][j][1], fa[i].x, fb[j].x);
-              dmma884(ci[i][j][0], ci[i][j][1], fa[i].x, fb[j].y);
-            }
-          }
-        }
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const double nai = -fa[i].y;
-          #pragma unroll
-          for (int j = 0; j < FN; ++j) {
-            if (j < jvalid) {
-              dmma884(cr[i][j][0], cr[i][j][1], nai, fb[j].y);
-              dmma884(ci[i][j][0], ci[i][j][1], fa[i].y, fb[j].x);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // refill the stage released one iteration ago with tile kt - 1 + STAGES: by now
-      // every warp has normally finished tile kt - 1, so this empty-barrier wait is
-      // almost always already complete and the producer lane does not stall its warp
-      // (waiting on the just-released stage cost ~8 % of warp samples, profiles/r01)
-      if (lane == 0 && kt >= kDefer && warp == (kt % NWARP) && kt - kDefer + STAGES < KT) {
-        mbar_wait(&empty[(kt - kDefer) % STAGES], ((kt - kDefer) / STAGES) & 1);
-        issue(kt - kDefer + STAGES);
-      }
-    }
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, true>(p, sA, sB, full, empty, issue, KT, wm, wn,
+                                                   lane, warp, fc, pr, jvalid, c0, c1, c2);
   }
 
   // epilogue: fragment row r <-> tile row perm8(r); fragment column c <-> perm8(c)
@@ -292,7 +290,14 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int t = 0; t < 2; ++t) {
         const int n = n0 + wn * WN + j * 8 + perm8(fc * 2 + t);
         if (n >= p.N) continue;
-        const double xr = cr[i][j][t], xi = ci[i][j][t];
+        double xr, xi;
+        if (MUL == 3) {
+          xr = c0[i][j][t] - c1[i][j][t];
+          xi = c2[i][j][t] - c0[i][j][t] - c1[i][j][t];
+        } else {
+          xr = c0[i][j][t];
+          xi = c1[i][j][t];
+        }
         if (EPI == EPI_PARTIAL) {
           p.ws[(long long)blockIdx.z * p.M * p.N + m + (long long)n * p.M] = make_double2(xr, xi);
         } else if (EPI == EPI_FILTER) {

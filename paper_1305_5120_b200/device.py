@@ -175,6 +175,15 @@ class Engine:
                      ptr(W), ld(W), int(panels), ctypes.byref(flag))
         return W if flag.value else Y
 
+    @staticmethod
+    def complex_mul():
+        """Complex-product scheme of the TMA GEMMs: 3 (3M) or 4 real products."""
+        return int(_native.load().chfsi_get_complex_mul())
+
+    @staticmethod
+    def set_complex_mul(mul):
+        _native.call("chfsi_set_complex_mul", int(mul))
+
     def filter_step(self, H, Y1, alpha, beta, Y0, gamma, C):
         n, k = rows(Y1), cols(Y1)
         _native.call("chfsi_filter_step", self.h, n, k, ptr(H), ld(H), ptr(Y1), ld(Y1),

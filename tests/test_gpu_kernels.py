@@ -375,7 +375,7 @@ def test_trtri_blocked_matches_inverse(eng):
 
 
 # every tile configuration and split factor the cost model can pick, on ragged shapes
-_NCFG = 11
+_NCFG = 14
 _TMA_FIRST = 7
 
 
@@ -420,6 +420,39 @@ def test_plan_is_tma_for_the_filter_shape(eng):
     _native.call("chfsi_gemm_plan", eng.h, 0, 0, 1, 20000, 2200, 20000, ctypes.byref(cfg),
                  ctypes.byref(split))
     assert cfg.value >= _TMA_FIRST and split.value == 1
+
+
+@pytest.mark.parametrize("mul", [3, 4])
+def test_complex_product_scheme(eng, mul):
+    """3M (Ar Br, Ai Bi, (Ar+Ai)(Br+Bi)) and four-product TMA kernels give the same
+    filter step and plain product to rounding, through the planner's own picks."""
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    rng = np.random.default_rng(40 + mul)
+    old = lib.chfsi_get_complex_mul()
+    try:
+        assert lib.chfsi_set_complex_mul(mul) == 0
+        assert lib.chfsi_get_complex_mul() == mul
+        for (n, k) in ((513, 26), (1000, 210), (2048, 64)):
+            H = crand(rng, n, n)
+            H = (H + H.conj().T) / 2
+            Y1, Y0 = crand(rng, n, k), crand(rng, n, k)
+            dY0 = D.to_device(Y0, eng.device)
+            eng.filter_step(D.to_device(H, eng.device), D.to_device(Y1, eng.device),
+                            0.7, -0.2, dY0, 0.1, dY0)
+            ref = 0.7 * (H @ Y1) - 0.2 * Y1 + 0.1 * Y0
+            assert np.linalg.norm(D.to_host(dY0) - ref) <= 1e-14 * np.linalg.norm(ref), (n, k)
+            dC = D.zeros(n, k, eng.device)
+            eng.zgemm("N", "N", n, k, n, 1.0, D.to_device(H, eng.device),
+                      D.to_device(Y1, eng.device), 0.0, dC)
+            ref = H @ Y1
+            err = np.abs(D.to_host(dC) - ref).max(axis=0)
+            # normwise per column: |C - HY|_max <= c eps ||H||_F ||y_j||
+            bound = 4e-16 * np.linalg.norm(H) * np.linalg.norm(Y1, axis=0)
+            assert np.all(err <= bound), (n, k, float((err / bound).max()))
+        assert lib.chfsi_set_complex_mul(5) != 0
+    finally:
+        lib.chfsi_set_complex_mul(old)
 
 
 def test_full_size_filter_on_exact_eigenvectors(eng):
