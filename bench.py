@@ -333,7 +333,7 @@ def run_b200(args, rank, world, local_rank):
             torch.cuda.empty_cache()
 
         leg("e2e", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev))
-        leg("tail", lambda: tail_widths(eng, H, n, dev))
+        leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
         del H, Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         leg("solve_c0", solve_c0)
@@ -363,6 +363,8 @@ KERNELS = {
     11: "zgemm_tma_kernel<64,32,warp32x16,TMA+mbarrier x4,EPI_FILTER,3M>",
     12: "zgemm_tma_kernel<64,32,warp16x32,TMA+mbarrier x4,EPI_FILTER,3M>",
     13: "zgemm_tma_kernel<64,32,warp16x16,TMA+mbarrier x4,EPI_FILTER,3M>",
+    14: "zgemm_tma_kernel<64,32,warp32x16,TMA+mbarrier x4,EPI_FILTER,3M,sum planes>",
+    15: "zgemm_tma_kernel<64,32,warp16x32,TMA+mbarrier x4,EPI_FILTER,3M,sum planes>",
 }
 
 
@@ -370,7 +372,8 @@ def plan_kernel_name(eng, n, k):
     import ctypes
     from paper_1305_5120_b200 import _native
     cfg, split = ctypes.c_int(), ctypes.c_int()
-    _native.call("chfsi_gemm_plan", eng.h, 0, 0, 1, n, k, n, ctypes.byref(cfg), ctypes.byref(split))
+    # filter_epilogue 2: the filter call's steps (3M operand-sum planes when 3M is on)
+    _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg), ctypes.byref(split))
     name = KERNELS.get(cfg.value, f"cfg{cfg.value}")
     return name + (f" split-K {split.value}" if split.value > 1 else "")
 
@@ -552,25 +555,29 @@ def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
             "path": "paper_1305_5120_b200.chebyshev_filter(H, Y, FilterSpec) -> VectorBlock.entries"}
 
 
-def tail_widths(eng, H, n, dev):
-    """Filter-step throughput at the solve's dominant narrow widths."""
+def tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref, degree=5):
+    """Filter throughput at the solve's dominant narrow widths: full
+    filter calls (sum planes, split-K plans) of `degree` steps; ms per step."""
     import torch
     out = {}
+    eng.declare_operator(H)  # as in a solve: H's 3M sum plane formed once, not per call
     for k in (26, 210, 275):
-        Y1 = torch.randn((k, n), dtype=torch.complex128, device=dev)
-        Y0 = torch.randn((k, n), dtype=torch.complex128, device=dev)
+        Y = torch.randn((k, n), dtype=torch.complex128, device=dev)
+        W = torch.empty_like(Y)
         for _ in range(2):
-            eng.filter_step(H, Y1, 0.5, -0.1, Y0, 0.2, Y0)
+            eng.filter(H, Y, W, degree, a_edge, b_up, lam_ref)
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
-        for _ in range(5):
-            eng.filter_step(H, Y1, 0.5, -0.1, Y0, 0.2, Y0)
+        for _ in range(3):
+            eng.filter(H, Y, W, degree, a_edge, b_up, lam_ref)
         b.record()
         torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / 5
-        out[str(k)] = {"ms": ms, "tflops": 8.0 * n * n * k / (ms * 1e-3) / 1e12}
+        ms = a.elapsed_time(b) / (3 * degree)
+        out[str(k)] = {"ms": ms, "tflops": 8.0 * n * n * k / (ms * 1e-3) / 1e12,
+                       "kernel": plan_kernel_name(eng, n, k)}
+    eng.declare_operator(None)
     return out
 
 

@@ -183,7 +183,9 @@ int chfsi_axpby(chfsi_handle_t h, int64_t n, int64_t k, double alpha_re, double 
                 int64_t ldy);
 
 /* Tuning hooks (process-wide): force GEMM tile config `cfg` (-1 = cost model) and
- * split-K factor (0 = automatic); query the plan the cost model picks for a shape. */
+ * split-K factor (0 = automatic); query the plan the cost model picks for a shape
+ * (filter_epilogue: 0 plain product, 1 fused filter step, 2 fused filter step of a
+ * chfsi_filter call, which supplies 3M operand-sum planes). */
 int chfsi_gemm_override(int cfg, int split);
 int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m,
                     int64_t n, int64_t k, int* h_cfg, int* h_split);
@@ -195,6 +197,14 @@ int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int
  * chfsi_get_complex_mul returns the current scheme. */
 int chfsi_set_complex_mul(int mul);
 int chfsi_get_complex_mul(void);
+
+/* Declare the n x n device operator d_H unchanged until the next declaration on this
+ * handle (d_H = NULL clears): its 3M sum plane (Re H + Im H, n^2 doubles of handle
+ * scratch) is computed once here and reused by every chfsi_filter call on the same
+ * (d_H, n, ldh) instead of once per call. A solve declares H for its duration
+ * (core.py:385-546 `chfsi_solve` filters the same H every outer iteration). Writing H
+ * while declared, without re-declaring, gives wrong filter results. */
+int chfsi_declare_operator(chfsi_handle_t h, int64_t n, const void* d_H, int64_t ldh);
 
 /* Microbenchmarks that give the roofline denominators on the box:
  * FP64 tensor-pipe (DMMA) and FP64 FMA-pipe (DFMA) peak, TFLOP/s. */

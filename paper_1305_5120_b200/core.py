@@ -492,6 +492,15 @@ class DeviceSolver:
 
     # -- driver -------------------------------------------------------
     def run(self, Y0, prior, rng, callback=None):
+        # H is not written during the solve: its 3M sum plane is formed once here instead
+        # of once per filter call (chfsi_declare_operator), and dropped at the end
+        self.eng.declare_operator(self.hb)
+        try:
+            return self._run(Y0, prior, rng, callback)
+        finally:
+            self.eng.declare_operator(None)
+
+    def _run(self, Y0, prior, rng, callback=None):
         cfg = self.cfg
         n, nev = self.n, cfg.nev
         s_tot = nev + cfg.buffer_cols

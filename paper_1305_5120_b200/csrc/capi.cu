@@ -446,12 +446,18 @@ int chfsi_gemm_override(int cfg, int split) { return gemm_override(cfg, split); 
 
 int chfsi_set_complex_mul(int mul) { return set_complex_mul(mul); }
 
+int chfsi_declare_operator(chfsi_handle_t h, int64_t n, const void* d_H, int64_t ldh) {
+  H_CHECK(h);
+  return declare_operator(h, n, (const double2*)d_H, ldh);
+}
+
 int chfsi_get_complex_mul(void) { return complex_mul(); }
 
 int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m, int64_t n,
                     int64_t k, int* h_cfg, int* h_split) {
   H_CHECK(h);
-  return gemm_plan(h, opa, opb, filter_epilogue ? 1 : 0, m, n, k, h_cfg, h_split);
+  return gemm_plan(h, opa, opb, filter_epilogue < 0 ? 0 : std::min(filter_epilogue, 2), m, n, k,
+                   h_cfg, h_split);
 }
 
 int chfsi_peak_dmma(int device, int iters, double* h_tflops) {

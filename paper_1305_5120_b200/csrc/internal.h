@@ -43,13 +43,17 @@ struct Handle {
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   // grow-only scratch arenas (stream-ordered reuse is safe: one stream)
-  static constexpr int kSlots = 9;
+  static constexpr int kSlots = 11;
   void* scratch[kSlots] = {nullptr};
   size_t scratch_bytes[kSlots] = {0};
   int* d_info = nullptr;
   double* h_pinned = nullptr;   // small pinned host staging
   size_t h_pinned_bytes = 0;
   int sm_count = 148;
+  // operator declared immutable by chfsi_declare_operator: its 3M sum plane (SLOT_HSUM)
+  // is reused by every filter call on the same (pointer, order, ld)
+  const void* op_ptr = nullptr;
+  long long op_n = 0, op_ld = 0;
   // launch counter: kernels this library launched since the last reset
   long long launches = 0;
   // CUDA-graph cache of filter calls (solver_ops.cu) and the split-K workspace
@@ -78,6 +82,8 @@ enum Slot : int {
   SLOT_TRI = 6,     // triangular-inverse temporaries
   SLOT_LANCZOS = 7, // Lanczos basis
   SLOT_COLRED = 8,  // per-column partial sums (split column reductions)
+  SLOT_HSUM = 9,    // 3M sum plane of the filter operator H (n x n doubles)
+  SLOT_YSUM = 10,   // 3M sum planes of the two rotating filter blocks (2 x n x k doubles)
 };
 
 void set_error(const std::string& msg);
@@ -117,16 +123,27 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
           double2* C, long long ldc, int tri = 0, long long tri_off = 0);
 // One fused Chebyshev degree step: C = alpha*A*Y1 + beta*Y1 + gamma*Y0 (Y0 may be null,
 // C may alias Y0). A is M x M, Y1/Y0/C are M x N.
+// 3M operand-sum planes (real, column-major, ld in doubles): As = Re A + Im A, Bs =
+// Re B + Im B; Cs (optional) receives Re C + Im C of the step's output.
+struct SumPlanes {
+  const double* As; long long ldas;
+  const double* Bs; long long ldbs;
+  double* Cs; long long ldcs;
+};
+int sum_plane(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
+              double* Xs, long long ldxs);
+int declare_operator(Handle* h, long long n, const double2* H, long long ldh);
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,
                       const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
-                      const double* coef_dev = nullptr);
+                      const double* coef_dev = nullptr, const SumPlanes* sp = nullptr);
 // Row panel of a fused step: rows [r0, r0 + M) of C = alpha*A*B + beta*Y1e + gamma*Y0
 // with A = H + r0 (M x K), B the full K x N block and Y1e = B + r0.
 int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const double2* A,
                        long long lda, const double2* B, long long ldb, const double2* Y1e,
                        long long ld1e, double alpha, double beta, const double2* Y0, long long ld0,
-                       double gamma, double2* C, long long ldc, const double* coef_dev);
+                       double gamma, double2* C, long long ldc, const double* coef_dev,
+                       const SumPlanes* sp = nullptr);
 // split-K workspace bytes the filter step's plan needs (pre-sized before graph capture)
 size_t filter_step_workspace(Handle* h, long long M, long long N);
 

@@ -275,6 +275,20 @@ __global__ void zaxpby_kernel(long long n, long long k, double2 alpha, const dou
   }
 }
 
+// 3M operand-sum plane Xs = Re X + Im X (HBM-bound: 16 B read + 8 B written per entry).
+__global__ void sum_plane_kernel(long long rows, long long cols, const double2* __restrict__ X,
+                                 long long ldx, double* __restrict__ Xs, long long ldxs) {
+  for (long long j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double2* x = X + j * ldx;
+    double* xs = Xs + j * ldxs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
+         i += (long long)gridDim.x * blockDim.x) {
+      const double2 v = x[i];
+      xs[i] = __dadd_rn(v.x, v.y);
+    }
+  }
+}
+
 __global__ void real_diag_kernel(long long n, const double2* A, long long lda, double* out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -438,6 +452,18 @@ int zaxpby_cols(Handle* h, long long n, long long k, double2 alpha, const double
                 long long ldx, double2 beta, double2* Y, long long ldy) {
   if (n * k <= 0) return OK;
   zaxpby_kernel<<<grid_for(n * k), 256, 0, h->stream>>>(n, k, alpha, X, ldx, beta, Y, ldy);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
+int sum_plane(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
+              double* Xs, long long ldxs) {
+  if (rows * cols <= 0) return OK;
+  const long long bx = std::min<long long>((rows + 255) / 256, 64);
+  const long long by = std::min<long long>(cols, 65535);
+  sum_plane_kernel<<<dim3((unsigned)bx, (unsigned)by), 256, 0, h->stream>>>(rows, cols, X, ldx, Xs,
+                                                                           ldxs);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;

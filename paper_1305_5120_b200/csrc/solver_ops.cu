@@ -113,16 +113,77 @@ static std::vector<double> filter_coefs(int degree, double a, double b, double l
   return coef;
 }
 
+// 3M operand-sum planes of one filter call (complex_mul() == 3): Hs = Re H + Im H and one
+// plane per rotating block (Y, W), ld rounded up to an even count (TMA strides are
+// multiples of 16 B). Each fused step reads the planes of H and of its input block and
+// writes the plane of its output from the epilogue, so no step adds DADDs to the DMMA
+// stream. nullptr when 3M is off or the block is empty.
+struct FilterSums {
+  double* Hs = nullptr;
+  double* Ys = nullptr;  // plane of Y (slot 0) and of W (slot 1)
+  double* Ws = nullptr;
+  long long ldh = 0, ldy = 0;
+};
+
+static int filter_sums(Handle* h, long long n, long long k, const double2* H, long long ldh,
+                       const double2* Y, long long ldy, FilterSums* fs) {
+  *fs = FilterSums{};
+  if (complex_mul() != 3 || n <= 0 || k <= 0) return OK;
+  const long long ld = (n + 1) & ~1LL;
+  fs->ldh = fs->ldy = ld;
+  // a declared operator (chfsi_declare_operator) keeps its plane across calls
+  const bool declared = h->op_ptr == (const void*)H && h->op_n == n && h->op_ld == ldh;
+  if (!declared) h->op_ptr = nullptr;  // the plane is about to be overwritten
+  fs->Hs = (double*)scratch(h, SLOT_HSUM, (size_t)ld * n * sizeof(double));
+  fs->Ys = (double*)scratch(h, SLOT_YSUM, (size_t)2 * ld * k * sizeof(double));
+  if (!fs->Hs || !fs->Ys) return ERR_NOMEM;
+  fs->Ws = fs->Ys + ld * k;
+  if (!declared) CHFSI_TRY(sum_plane(h, n, n, H, ldh, fs->Hs, ld));
+  return sum_plane(h, n, k, Y, ldy, fs->Ys, ld);
+}
+
+// chfsi_declare_operator: H stays unchanged until the next declaration (or a clear with
+// H = nullptr); its sum plane is computed now and reused by the filter calls on it.
+int declare_operator(Handle* h, long long n, const double2* H, long long ldh) {
+  h->op_ptr = nullptr;
+  h->op_n = h->op_ld = 0;
+  if (H == nullptr || n <= 0 || complex_mul() != 3) return OK;
+  if (ldh < n) {
+    set_error("declare_operator: ldh must be >= n");
+    return ERR_ARG;
+  }
+  const long long ld = (n + 1) & ~1LL;
+  double* hs = (double*)scratch(h, SLOT_HSUM, (size_t)ld * n * sizeof(double));
+  if (!hs) return ERR_NOMEM;
+  CHFSI_TRY(sum_plane(h, n, n, H, ldh, hs, ld));
+  h->op_ptr = H;
+  h->op_n = n;
+  h->op_ld = ldh;
+  return OK;
+}
+
 // Degree steps j0 .. degree-1 (step j0 - 1 left its result in `cur`, its input in `prev`).
 static int filter_steps(Handle* h, long long n, long long k, int degree, int j0, const double* coef,
                         const double* coef_dev, const double2* H, long long ldh, double2* prev,
                         long long ldp, double2* cur, long long ldc, double2* W,
-                        int* result_in_w) {
+                        int* result_in_w, const FilterSums* fs = nullptr) {
+  // sum planes follow their blocks: after step j0 - 1 the output (cur) is W iff j0 is odd
+  const bool sums = fs != nullptr && fs->Hs != nullptr;
+  double* s_prev = nullptr;
+  double* s_cur = nullptr;
+  if (sums) {
+    s_cur = (cur == W) ? fs->Ws : fs->Ys;
+    s_prev = (cur == W) ? fs->Ys : fs->Ws;
+  }
   for (int j = j0; j < degree; ++j) {
+    SumPlanes sp{fs ? fs->Hs : nullptr, fs ? fs->ldh : 0, s_cur, fs ? fs->ldy : 0, s_prev,
+                 fs ? fs->ldy : 0};
     CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, cur, ldc, coef[3 * j], coef[3 * j + 1], prev, ldp,
-                                coef[3 * j + 2], prev, ldp, coef_dev ? coef_dev + 3 * j : nullptr));
+                                coef[3 * j + 2], prev, ldp, coef_dev ? coef_dev + 3 * j : nullptr,
+                                sums ? &sp : nullptr));
     std::swap(prev, cur);
     std::swap(ldp, ldc);
+    std::swap(s_prev, s_cur);
   }
   *result_in_w = (cur == W) ? 1 : 0;
   return OK;
@@ -146,9 +207,14 @@ int filter(Handle* h, long long n, long long k, int degree, double a, double b, 
 static int filter_issue(Handle* h, long long n, long long k, int degree, const double* coef,
                         const double* coef_dev, const double2* H, long long ldh, double2* Y,
                         long long ldy, double2* W, long long ldw, int* result_in_w) {
+  // graph capture (coef_dev) keeps the plain kernels: no scratch growth inside a capture
+  FilterSums fs;
+  if (coef_dev == nullptr) CHFSI_TRY(filter_sums(h, n, k, H, ldh, Y, ldy, &fs));
+  SumPlanes sp{fs.Hs, fs.ldh, fs.Ys, fs.ldy, fs.Ws, fs.ldy};
   CHFSI_TRY(zgemm_filter_step(h, n, k, H, ldh, Y, ldy, coef[0], coef[1], nullptr, 0, 0.0, W, ldw,
-                              coef_dev));
-  return filter_steps(h, n, k, degree, 1, coef, coef_dev, H, ldh, Y, ldy, W, ldw, W, result_in_w);
+                              coef_dev, fs.Hs ? &sp : nullptr));
+  return filter_steps(h, n, k, degree, 1, coef, coef_dev, H, ldh, Y, ldy, W, ldw, W, result_in_w,
+                      &fs);
 }
 
 // Filter whose operator arrives from host memory (core.py:287-311 `chebyshev_filter`
@@ -175,6 +241,7 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     set_error("filter_streamed: leading dimensions must be >= n");
     return ERR_ARG;
   }
+  if (h->op_ptr == (const void*)H) h->op_ptr = nullptr;  // H is rewritten below
   if (panels <= 0) panels = n >= 8192 ? 8 : (n >= 2048 ? 4 : 1);
   // panel height: a multiple of 64 rows (the CTA tile height)
   long long rows = (n + panels - 1) / panels;
@@ -207,8 +274,12 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0], coef[1],
                                  nullptr, 0, 0.0, W + r0, ldw, nullptr));
   }
+  // 3M sum planes once all of H is in: Hs and the plane of the first step's output W
+  FilterSums fs;
+  CHFSI_TRY(filter_sums(h, n, k, H, ldh, W, ldw, &fs));
+  std::swap(fs.Ys, fs.Ws);
   CHFSI_TRY(filter_steps(h, n, k, degree, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, W,
-                         result_in_w));
+                         result_in_w, &fs));
   // everything is queued; return once the host buffer has been read so the caller
   // may free or reuse it (the GPU keeps filtering meanwhile)
   CHFSI_CUDA(cudaEventSynchronize(ev[panels - 1]));

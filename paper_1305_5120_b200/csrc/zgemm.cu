@@ -25,7 +25,7 @@ __global__ void zgemm_splitk_reduce_kernel(int M, int N, int S, const double2* _
                                            int epi, double2 alpha, double2 beta, double2* C,
                                            long long ldc, const double2* Y1, long long ld1,
                                            const double2* Y0, long long ld0, double gamma,
-                                           const double* coef) {
+                                           const double* coef, double* Cs, long long ldcs) {
   if (coef != nullptr) {  // graph-replayed filter step: coefficients live on the device
     alpha.x = coef[0];
     beta.x = coef[1];
@@ -44,14 +44,15 @@ __global__ void zgemm_splitk_reduce_kernel(int M, int N, int S, const double2* _
     }
     if (epi == EPI_FILTER) {
       const double2 y1 = Y1[m + n * ld1];
-      double orr = alpha.x * xr + beta.x * y1.x;
-      double oi = alpha.x * xi + beta.x * y1.y;
+      double orr = __fma_rn(alpha.x, xr, __dmul_rn(beta.x, y1.x));
+      double oi = __fma_rn(alpha.x, xi, __dmul_rn(beta.x, y1.y));
       if (Y0 != nullptr) {
         const double2 y0 = Y0[m + n * ld0];
-        orr += gamma * y0.x;
-        oi += gamma * y0.y;
+        orr = __fma_rn(gamma, y0.x, orr);
+        oi = __fma_rn(gamma, y0.y, oi);
       }
       C[m + n * ldc] = make_double2(orr, oi);
+      if (Cs != nullptr) Cs[m + n * ldcs] = __dadd_rn(orr, oi);
     } else {
       double2 o = make_double2(alpha.x * xr - alpha.y * xi, alpha.x * xi + alpha.y * xr);
       if (beta.x != 0.0 || beta.y != 0.0) {
@@ -60,6 +61,7 @@ __global__ void zgemm_splitk_reduce_kernel(int M, int N, int S, const double2* _
         o.y += beta.x * c.y + beta.y * c.x;
       }
       C[m + n * ldc] = o;
+      if (Cs != nullptr) Cs[m + n * ldcs] = __dadd_rn(o.x, o.y);
     }
   }
 }
@@ -85,9 +87,10 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 14;
+constexpr int NCFG = 16;
 constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
 constexpr int FIRST_3M = 11;  // cfgs >= 11: the TMA kernels with 3M complex products
+constexpr int FIRST_SUMS = 14;  // cfgs >= 14: 3M reading precomputed operand-sum planes
 // cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
 // cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
 // cfg 2: 64x16   BK8  warp 16x16 (4 warps)     cfg 6: 128x32 BK8  warp 32x16 (8 warps)
@@ -102,13 +105,14 @@ using C6 = CfgT<128, 32, 8, 32, 16, 4>;
 // cfg 7: TMA 64x32 warp 32x16, 4 stages; cfg 8: TMA 64x16 warp 16x16; cfg 9: TMA 64x64 warp 32x32
 // cfg 10: TMA 64x32 with four 16x32 warps stacked by rows (same fragment loads per DMMA as
 // cfg 7; on a ragged column edge every warp keeps the same number of live 8-column blocks)
-using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const GemmParams);
-template <int BM, int BN, int WM, int WN, int ST, int MINB = 1, int MUL = 4>
+using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                      const CUtensorMap, const GemmParams);
+template <int BM, int BN, int WM, int WN, int ST, int MINB = 1, int MUL = 4, bool SUMS = false>
 struct TmaT {
   static constexpr int threads = (BM / WM) * (BN / WN) * 32;
-  static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST>(); }
+  static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST, SUMS>(); }
   template <int EPI>
-  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB, MUL>; }
+  static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB, MUL, SUMS>; }
 };
 // (explicit min-blocks keep ptxas at <= 128 regs -> 4 CTAs / SM for the 64x32 tile;
 // a register-double-buffered fragment variant measured 1.5-2 % slower, profiles/r01)
@@ -122,10 +126,13 @@ using T11 = TmaT<64, 32, 32, 16, 4, 3, 3>;
 using T12 = TmaT<64, 32, 16, 32, 4, 3, 3>;
 // cfg 13: 3M, 64x32 with eight 16x16 warps (24 accumulator doubles: 2 CTAs / SM = 16 warps)
 using T13 = TmaT<64, 32, 16, 16, 4, 2, 3>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8};
-const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16};  // warp tile width
+// cfg 14 / 15: cfg 11 / 12 reading precomputed operand-sum planes (3M without in-loop DADDs)
+using T14 = TmaT<64, 32, 32, 16, 4, 3, 3, true>;
+using T15 = TmaT<64, 32, 16, 32, 4, 3, 3, true>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32, 32, 32};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8};
+const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16, 16, 32};  // warp tile width
 bool g_tma_enabled = true;
 // complex products in the TMA kernels: 3 (3M, default) or 4 real DMMA products
 int g_mul = [] {
@@ -188,6 +195,8 @@ int ensure_table() {
   put_tma<T11>(11);
   put_tma<T12>(12);
   put_tma<T13>(13);
+  put_tma<T14>(14);
+  put_tma<T15>(15);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -230,7 +239,7 @@ struct Plan {
 //     warps (ncu: DMMA pipe 92.5 % vs 95.7 % active at k = 210): x (1 + kRag / tiles_n);
 //   * split-K adds the reduce pass: kTred + (s + 3) M N 16 B at HBM speed.
 constexpr double kEffNN[NCFG] = {0.906, 0.898, 0.837, 0.823, 0.911, 0.926, 0.885,
-                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13};
+                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13, 1.27, 1.26};
 constexpr double kEffCN[7] = {0.886, 0.927, 0.877, 0.854, 1.058, 0.971, 0.887};
 constexpr double kR0Warps4 = 1.289, kR0Warps8 = 1.108;
 constexpr double kRag = 0.122, kFloor = 0.859;
@@ -269,7 +278,8 @@ double plan_cost(int c, int occ, int threads, bool nn, int sms, long long M, lon
   return t;
 }
 
-Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
+Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+            bool sums) {
   Plan best;
   double best_cost = 1e300;
   const int sms = h->sm_count;
@@ -278,6 +288,12 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
     if (c >= FIRST_TMA && !g_tma_enabled) continue;
     if (g_force_cfg < 0 && c >= FIRST_TMA && (c >= FIRST_3M) != (g_mul == 3)) continue;
+    // 3M on: every op N x N product runs a 3M kernel (the cp.async kernels use four
+    // products), so the rounding of a product does not depend on the planner's pick
+    if (g_force_cfg < 0 && nn && g_mul == 3 && g_tma_enabled && K > 0 && c < FIRST_3M) continue;
+    // operand-sum planes: only (and always) the sum-reading kernels; never without planes
+    if (c >= FIRST_SUMS && !sums && g_force_cfg < 0) continue;
+    if (g_force_cfg < 0 && sums && c < FIRST_SUMS) continue;
     const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
     if (!e.ready && !ep.ready) continue;
@@ -309,11 +325,11 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
 // per-call host cost of a small GEMM is a hash lookup (the solve's tail issues
 // thousands of identical small products).
 struct PlanKey {
-  int opa, opb, epi, fcfg, fsplit, mul;
+  int opa, opb, epi, fcfg, fsplit, mul, sums;
   long long M, N, K;
   bool operator==(const PlanKey& o) const {
     return opa == o.opa && opb == o.opb && epi == o.epi && fcfg == o.fcfg && fsplit == o.fsplit &&
-           mul == o.mul &&
+           mul == o.mul && sums == o.sums &&
            M == o.M && N == o.N && K == o.K;
   }
 };
@@ -322,17 +338,19 @@ struct PlanKeyHash {
     size_t h = (size_t)k.M * 0x9E3779B97F4A7C15ULL;
     h ^= (size_t)k.N * 0xC2B2AE3D27D4EB4FULL + (h << 6) + (h >> 2);
     h ^= (size_t)k.K * 0x165667B19E3779F9ULL + (h << 6) + (h >> 2);
-    h ^= (size_t)(k.opa | (k.opb << 1) | (k.epi << 2) | ((k.fcfg + 1) << 4) | (k.fsplit << 9));
+    h ^= (size_t)(k.opa | (k.opb << 1) | (k.epi << 2) | ((k.fcfg + 1) << 4) | (k.fsplit << 9) |
+                  (k.mul << 16) | (k.sums << 20));
     return h;
   }
 };
 
-Plan cached_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K) {
+Plan cached_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+                 bool sums) {
   static std::unordered_map<PlanKey, Plan, PlanKeyHash> cache;
-  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, g_mul, M, N, K};
+  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, g_mul, sums ? 1 : 0, M, N, K};
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  const Plan pl = choose(h, opa, opb, epi, M, N, K, sums);
   if (cache.size() > 65536) cache.clear();
   cache.emplace(key, pl);
   return pl;
@@ -374,20 +392,54 @@ int encode_colmajor(CUtensorMap* map, const double2* base, long long rows, long 
   return OK;
 }
 
+// Real column-major plane (rows x cols doubles, ld) as a 2-D FP64 tensor, box
+// {box_rows, box_cols}; 64-byte swizzle for the Bs tile (conflict-free fragment reads).
+int encode_real(CUtensorMap* map, const double* base, long long rows, long long cols, long long ld,
+                int box_rows, int box_cols, bool swizzle64) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled entry point unavailable");
+    return ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         swizzle64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (sum plane) failed: " + std::to_string((int)r));
+    return ERR_CUDA;
+  }
+  return OK;
+}
+
 int run_kernel(Handle* h, int c, const Entry& e, dim3 grid, const GemmParams& p) {
   if (!e.tma) {
     e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
   } else {
     // A: M x K (8-row boxes, BK = 8 columns); B: K x N (BK rows, BN columns)
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mas, mbs;
     CHFSI_TRY(encode_colmajor(&ma, p.A, p.M, p.K, p.lda, 8, kBKc[c]));
     CHFSI_TRY(encode_colmajor(&mb, p.B, p.K, p.N, p.ldb, kBKc[c], kBN[c]));
-    reinterpret_cast<TmaFn>(e.fn)<<<grid, e.threads, e.smem, h->stream>>>(ma, mb, p);
+    if (c >= FIRST_SUMS) {
+      CHFSI_TRY(encode_real(&mas, p.As, p.M, p.K, p.ldas, 8, kBKc[c], false));
+      CHFSI_TRY(encode_real(&mbs, p.Bs, p.K, p.N, p.ldbs, kBKc[c], kBN[c], true));
+    } else {
+      mas = ma;
+      mbs = mb;
+    }
+    reinterpret_cast<TmaFn>(e.fn)<<<grid, e.threads, e.smem, h->stream>>>(ma, mb, mas, mbs, p);
   }
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;
 }
+
+int launch_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+                GemmParams p, const Plan& pl);
 
 int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
            GemmParams p) {
@@ -400,7 +452,29 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
-  const Plan pl = cached_plan(h, opa, opb, epi, M, N, K);
+  const bool sums = p.As != nullptr && p.Bs != nullptr && g_mul == 3 && opa == OP_N &&
+                    opb == OP_N && g_tma_enabled;
+  const Plan pl = cached_plan(h, opa, opb, epi, M, N, K, sums);
+  const int c = pl.cfg;
+  if (c >= FIRST_SUMS && !sums) {
+    set_error("zgemm: forced config " + std::to_string(c) + " needs operand sum planes");
+    return ERR_ARG;
+  }
+  // a kernel that does not read the planes (forced config, 4 products, TMA off) leaves
+  // the output plane to a separate pass after the product
+  double* cs_after = nullptr;
+  if (c < FIRST_SUMS) {
+    p.As = p.Bs = nullptr;
+    cs_after = p.Cs;
+    p.Cs = nullptr;
+  }
+  CHFSI_TRY(launch_plan(h, opa, opb, epi, M, N, K, p, pl));
+  if (cs_after != nullptr) CHFSI_TRY(sum_plane(h, M, N, p.C, p.ldc, cs_after, p.ldcs));
+  return OK;
+}
+
+int launch_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
+                GemmParams p, const Plan& pl) {
   const int c = pl.cfg;
   p.tiles_m = (int)((M + kBM[c] - 1) / kBM[c]);
   p.tiles_n = (int)((N + kBN[c] - 1) / kBN[c]);
@@ -443,7 +517,7 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   const int blocks = (int)std::min<long long>((total + threads - 1) / threads, 148LL * 16);
   zgemm_splitk_reduce_kernel<<<blocks, threads, 0, h->stream>>>(
       (int)M, (int)N, pl.split, ws, epi, p.alpha, p.beta, p.C, p.ldc, p.Y1e, p.ld1e, p.Y0, p.ld0,
-      p.gamma, epi == EPI_FILTER ? p.coef : nullptr);
+      p.gamma, epi == EPI_FILTER ? p.coef : nullptr, p.Cs, p.ldcs);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;
@@ -480,7 +554,8 @@ void gemm_overrides(int* cfg, int* split) {
 int gemm_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
               int* cfg, int* split) {
   CHFSI_TRY(ensure_table());
-  const Plan pl = choose(h, opa, opb, epi, M, N, K);
+  const bool sums = epi == 2 && g_mul == 3 && opa == OP_N && opb == OP_N && g_tma_enabled;
+  const Plan pl = choose(h, opa, opb, epi ? EPI_FILTER : EPI_STORE, M, N, K, sums);
   *cfg = pl.cfg;
   *split = pl.split;
   return OK;
@@ -528,8 +603,14 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
 int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const double2* A,
                        long long lda, const double2* B, long long ldb, const double2* Y1e,
                        long long ld1e, double alpha, double beta, const double2* Y0, long long ld0,
-                       double gamma, double2* C, long long ldc, const double* coef_dev) {
+                       double gamma, double2* C, long long ldc, const double* coef_dev,
+                       const SumPlanes* sp) {
   GemmParams p{};
+  if (sp != nullptr) {
+    p.As = sp->As; p.ldas = sp->ldas;
+    p.Bs = sp->Bs; p.ldbs = sp->ldbs;
+    p.Cs = sp->Cs; p.ldcs = sp->ldcs;
+  }
   p.A = A; p.lda = lda;
   p.B = B; p.ldb = ldb;
   p.C = C; p.ldc = ldc;
@@ -544,14 +625,14 @@ int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const d
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,
                       const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,
-                      const double* coef_dev) {
+                      const double* coef_dev, const SumPlanes* sp) {
   return zgemm_filter_panel(h, M, N, M, A, lda, Y1, ld1, Y1, ld1, alpha, beta, Y0, ld0, gamma, C,
-                            ldc, coef_dev);
+                            ldc, coef_dev, sp);
 }
 
 size_t filter_step_workspace(Handle* h, long long M, long long N) {
   if (ensure_table() != OK) return 0;
-  const Plan pl = cached_plan(h, OP_N, OP_N, EPI_FILTER, M, N, M);
+  const Plan pl = cached_plan(h, OP_N, OP_N, EPI_FILTER, M, N, M, false);
   return pl.split > 1 ? (size_t)pl.split * M * N * sizeof(double2) : 0;
 }
 

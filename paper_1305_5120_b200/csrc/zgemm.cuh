@@ -51,6 +51,12 @@ struct GemmParams {
   // shard of L^-1 A L^-H multiplies by rows [tri_off, tri_off + N) of L^-1).
   int tri;
   int tri_off;
+  // 3M operand-sum planes (real, column-major; ld in doubles): As = Re A + Im A (M x K),
+  // Bs = Re B + Im B (K x N); Cs (optional, EPI_FILTER / EPI_STORE of the TMA kernels and
+  // the split-K reduce) receives Re C + Im C of the result, the next step's Bs
+  const double* As; long long ldas;
+  const double* Bs; long long ldbs;
+  double* Cs; long long ldcs;
 };
 
 __device__ __forceinline__ void tri_krange(const GemmParams& p, int m0, int n0, int bm, int bn,

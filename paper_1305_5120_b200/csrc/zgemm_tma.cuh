@@ -80,6 +80,12 @@ __device__ __forceinline__ double2 lds128(unsigned addr) {
   return v;
 }
 
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); }
 
 // Stage refill lag: at k-tile kt the producer lane refills the stage of tile
@@ -92,9 +98,10 @@ constexpr int kDefer = CHFSI_TMA_DEFER;
 // One k-tile sweep per stage: wait for the stage, run the BK/4 DMMA k-steps of the
 // warp tile, release the stage, and (rotating producer lane) refill the stage that
 // was released one iteration earlier.
-template <int BM, int BN, int WM, int WN, int STAGES, int MUL, bool RAGGED, class Issue>
+template <int BM, int BN, int WM, int WN, int STAGES, int MUL, bool SUMS, bool RAGGED, class Issue>
 __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2* sA,
-                                             const double2* sB, uint64_t* full, uint64_t* empty,
+                                             const double2* sB, const double* sAs,
+                                             const double* sBs, uint64_t* full, uint64_t* empty,
                                              Issue& issue, int KT, int wm, int wn, int lane,
                                              int warp, int fc, int pr, int jvalid,
                                              double (&c0)[WM / 8][WN / 8][2],
@@ -113,6 +120,8 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
     // registers, shorter load-to-use latency)
     const unsigned a = smem_u32(sA + s * A_ELEMS);
     const unsigned b = smem_u32(sB + s * B_ELEMS);
+    const unsigned as_base = SUMS ? smem_u32(sAs + s * A_ELEMS) : 0u;
+    const unsigned bs_base = SUMS ? smem_u32(sBs + s * B_ELEMS) : 0u;
     #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       const int kk = ks * 4 + fc;
@@ -131,10 +140,26 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
         // 3M: three real products per complex MAC. The operand sums cost FM + FN DADDs
         // per 3 FM FN DMMAs.
         double as[FM], bs[FN];
-        #pragma unroll
-        for (int i = 0; i < FM; ++i) as[i] = fa[i].x + fa[i].y;
-        #pragma unroll
-        for (int j = 0; j < FN; ++j) bs[j] = fb[j].x + fb[j].y;
+        if (SUMS) {
+          // precomputed operand sums: As box g = {8 rows, BK cols} unswizzled (64 B per
+          // column), Bs = {BK rows, BN cols} with 64-byte swizzle; both conflict-free
+          #pragma unroll
+          for (int i = 0; i < FM; ++i) {
+            const int mg = (wm * WM) / 8 + i;
+            as[i] = lds64(as_base + 8u * (mg * 64 + kk * 8 + pr));
+          }
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            const int nn = wn * WN + j * 8 + pr;
+            const unsigned off = 64u * nn + 8u * kk;
+            bs[j] = lds64(bs_base + (off ^ (((off >> 7) & 3u) << 4)));
+          }
+        } else {
+          #pragma unroll
+          for (int i = 0; i < FM; ++i) as[i] = fa[i].x + fa[i].y;
+          #pragma unroll
+          for (int j = 0; j < FN; ++j) bs[j] = fb[j].x + fb[j].y;
+        }
         #pragma unroll
         for (int i = 0; i < FM; ++i)
           #pragma unroll
@@ -184,21 +209,29 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
   }
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES>
+template <int BM, int BN, int WM, int WN, int STAGES, bool SUMS = false>
 constexpr int zgemm_tma_smem_bytes() {
-  return STAGES * (BM * 8 + BN * 8) * 16 + 1024 /* alignment slack */ + 2 * STAGES * 8;
+  return STAGES * (BM * 8 + BN * 8) * (SUMS ? 24 : 16) + 1024 /* alignment slack */ +
+         2 * STAGES * 8;
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1, int MUL = 4>
+// MUL = 4: four real products per complex MAC; MUL = 3: 3M. SUMS (3M only): the operand
+// sums Ar + Ai and Br + Bi arrive precomputed as real planes (p.As, p.Bs; maps mapAs,
+// mapBs), so the main loop issues no DADDs (an in-loop DADD stalls the DMMA stream:
+// ncu, DMMA pipe 88.6 % active with in-loop sums vs 95.8 % without).
+template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1, int MUL = 4,
+          bool SUMS = false>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                 const GemmParams p) {
+                 const __grid_constant__ CUtensorMap mapAs,
+                 const __grid_constant__ CUtensorMap mapBs, const GemmParams p) {
+  static_assert(!SUMS || MUL == 3, "operand sums are a 3M feature");
   constexpr int BK = 8;
   constexpr int NWM = BM / WM;
   constexpr int NWARP = NWM * (BN / WN);
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
-  constexpr unsigned STAGE_BYTES = (A_ELEMS + B_ELEMS) * 16;
+  constexpr unsigned STAGE_BYTES = (A_ELEMS + B_ELEMS) * (SUMS ? 24 : 16);
   static_assert((A_ELEMS * 16) % 1024 == 0 && (B_ELEMS * 16) % 1024 == 0, "1 KB aligned tiles");
 
   extern __shared__ unsigned char smem_raw[];
@@ -206,7 +239,10 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double2* sA = base;
   double2* sB = base + STAGES * A_ELEMS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_ELEMS);
+  double* sAs = reinterpret_cast<double*>(sB + STAGES * B_ELEMS);  // SUMS only
+  double* sBs = sAs + STAGES * A_ELEMS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(SUMS ? reinterpret_cast<void*>(sBs + STAGES * B_ELEMS)
+                                                    : reinterpret_cast<void*>(sAs));
   uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -232,6 +268,10 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    if (SUMS) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapAs)) : "memory");
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapBs)) : "memory");
+    }
   }
   __syncthreads();
 
@@ -245,6 +285,12 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int g = 0; g < BM / 8; ++g)
       tma_load_2d(sA + s * A_ELEMS + g * BK * 8, &mapA, 2 * (m0 + 8 * g), k0, &full[s]);
     tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
+    if (SUMS) {
+      #pragma unroll
+      for (int g = 0; g < BM / 8; ++g)
+        tma_load_2d(sAs + s * A_ELEMS + g * BK * 8, &mapAs, m0 + 8 * g, k0, &full[s]);
+      tma_load_2d(sBs + s * B_ELEMS, &mapBs, k0, n0, &full[s]);
+    }
   };
 
   if (tid == 0) {
@@ -272,10 +318,10 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int t = 0; t < 2; ++t) c0[i][j][t] = c1[i][j][t] = c2[i][j][t] = 0.0;
 
   if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, false>(p, sA, sB, full, empty, issue, KT, wm, wn,
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, false>(p, sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                     lane, warp, fc, pr, jvalid, c0, c1, c2);
   } else {  // ragged column edge: skip 8-column blocks past N
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, true>(p, sA, sB, full, empty, issue, KT, wm, wn,
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, true>(p, sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                    lane, warp, fc, pr, jvalid, c0, c1, c2);
   }
 
@@ -290,10 +336,13 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int t = 0; t < 2; ++t) {
         const int n = n0 + wn * WN + j * 8 + perm8(fc * 2 + t);
         if (n >= p.N) continue;
+        // explicit roundings (no contraction choices left to the compiler): every
+        // instantiation -- tile shape, sum planes or not -- rounds the same way, so a
+        // product is bit-identical whichever config the planner picks without split-K
         double xr, xi;
         if (MUL == 3) {
-          xr = c0[i][j][t] - c1[i][j][t];
-          xi = c2[i][j][t] - c0[i][j][t] - c1[i][j][t];
+          xr = __dsub_rn(c0[i][j][t], c1[i][j][t]);
+          xi = __dsub_rn(__dsub_rn(c2[i][j][t], c0[i][j][t]), c1[i][j][t]);
         } else {
           xr = c0[i][j][t];
           xi = c1[i][j][t];
@@ -304,14 +353,15 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           double fa, fb, fg;
           filter_coef(p, fa, fb, fg);
           const double2 y1 = p.Y1e[m + (long long)n * p.ld1e];
-          double orr = fa * xr + fb * y1.x;
-          double oi = fa * xi + fb * y1.y;
+          double orr = __fma_rn(fa, xr, __dmul_rn(fb, y1.x));
+          double oi = __fma_rn(fa, xi, __dmul_rn(fb, y1.y));
           if (p.Y0 != nullptr) {
             const double2 y0 = p.Y0[m + (long long)n * p.ld0];
-            orr += fg * y0.x;
-            oi += fg * y0.y;
+            orr = __fma_rn(fg, y0.x, orr);
+            oi = __fma_rn(fg, y0.y, oi);
           }
           p.C[m + (long long)n * p.ldc] = make_double2(orr, oi);
+          if (p.Cs != nullptr) p.Cs[m + (long long)n * p.ldcs] = __dadd_rn(orr, oi);
         } else {
           double2 o = make_double2(p.alpha.x * xr - p.alpha.y * xi, p.alpha.x * xi + p.alpha.y * xr);
           if (p.beta.x != 0.0 || p.beta.y != 0.0) {
@@ -320,6 +370,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
             o.y += p.beta.x * c.y + p.beta.y * c.x;
           }
           p.C[m + (long long)n * p.ldc] = o;
+          if (p.Cs != nullptr) p.Cs[m + (long long)n * p.ldcs] = __dadd_rn(o.x, o.y);
         }
       }
     }

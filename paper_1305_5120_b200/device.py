@@ -184,6 +184,14 @@ class Engine:
     def set_complex_mul(mul):
         _native.call("chfsi_set_complex_mul", int(mul))
 
+    def declare_operator(self, H):
+        """H (device, n x n) stays unchanged until the next declaration; None clears.
+        Filter calls on it reuse its 3M sum plane (chfsi_declare_operator)."""
+        if H is None:
+            _native.call("chfsi_declare_operator", self.h, 0, ctypes.c_void_p(0), 0)
+        else:
+            _native.call("chfsi_declare_operator", self.h, rows(H), ptr(H), ld(H))
+
     def filter_step(self, H, Y1, alpha, beta, Y0, gamma, C):
         n, k = rows(Y1), cols(Y1)
         _native.call("chfsi_filter_step", self.h, n, k, ptr(H), ld(H), ptr(Y1), ld(Y1),

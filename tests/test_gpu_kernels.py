@@ -375,11 +375,12 @@ def test_trtri_blocked_matches_inverse(eng):
 
 
 # every tile configuration and split factor the cost model can pick, on ragged shapes
-_NCFG = 14
+_NCFG = 16
 _TMA_FIRST = 7
+_SUMS_FIRST = 14  # 3M kernels reading operand-sum planes: filter calls only
 
 
-@pytest.mark.parametrize("cfg", list(range(_NCFG)))
+@pytest.mark.parametrize("cfg", list(range(_SUMS_FIRST)))
 @pytest.mark.parametrize("split", [1, 3])
 def test_every_gemm_config_and_split(eng, cfg, split):
     from paper_1305_5120_b200 import _native, device as D
@@ -409,6 +410,47 @@ def test_every_gemm_config_and_split(eng, cfg, split):
                                 0.7, -0.2, dY0, 0.1, dY0)
                 ref = 0.7 * (H @ Y1) - 0.2 * Y1 + 0.1 * Y0
                 assert np.linalg.norm(D.to_host(dY0) - ref) <= 1e-13 * np.linalg.norm(ref)
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
+@pytest.mark.parametrize("cfg", [-1, _SUMS_FIRST, _SUMS_FIRST + 1, 7, 11])
+@pytest.mark.parametrize("split", [0, 1, 3])
+def test_filter_with_sum_planes(eng, cfg, split):
+    """chfsi_filter with 3M operand-sum planes (Hs, and per block the plane its step's
+    epilogue or split-K reduce wrote): every sum-reading config and split against the
+    oracle recurrence, ragged n and k; a forced config that reads no planes (7, 11) still
+    leaves correct planes for the next step (separate sum pass)."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import _native, device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    lib = _native.load()
+    try:
+        assert lib.chfsi_gemm_override(cfg, split) == 0
+        for (n, k, m) in ((301, 37, 6), (1000, 120, 5), (130, 1, 3)):
+            h, lam, _ = baseline_matrix(n, n)
+            rng = np.random.default_rng(n + k + cfg)
+            y = crand(rng, n, k)
+            a, b, lam_ref = float(lam[min(k, n - 1)]), float(lam[-1]) * 1.05, float(lam[0])
+            ref = O.cheb_filter(h, y, m, a, b, lam_ref)
+            dW = D.zeros(n, k, eng.device)
+            got = D.to_host(eng.filter(D.to_device(h, eng.device), D.to_device(y, eng.device),
+                                       dW, m, a, b, lam_ref))
+            assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref), (n, k, m)
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
+def test_sum_config_needs_planes(eng):
+    """Forcing a sum-reading config on a product without planes is an argument error."""
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    try:
+        assert lib.chfsi_gemm_override(_SUMS_FIRST, 1) == 0
+        x = D.zeros(64, 64, eng.device)
+        st = lib.chfsi_zgemm(eng.h, 0, 0, 64, 64, 64, 1.0, 0.0, D.ptr(x), 64, D.ptr(x), 64, 0.0,
+                             0.0, D.ptr(x), 64)
+        assert st != 0 and b"sum planes" in lib.chfsi_last_error()
     finally:
         lib.chfsi_gemm_override(-1, 0)
 
