@@ -126,12 +126,14 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
 // 3M operand-sum planes (real, column-major, ld in doubles): As = Re A + Im A, Bs =
 // Re B + Im B; Cs (optional) receives Re C + Im C of the step's output.
 struct SumPlanes {
-  const double* As; long long ldas;
+  const double* As; long long ldas;  // As grouped (zgemm.cuh), ldas unused
   const double* Bs; long long ldbs;
   double* Cs; long long ldcs;
 };
 int sum_plane(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
               double* Xs, long long ldxs);
+int sum_plane_grouped(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
+                      double* Xs);
 int declare_operator(Handle* h, long long n, const double2* H, long long ldh);
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,

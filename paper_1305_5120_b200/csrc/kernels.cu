@@ -289,6 +289,21 @@ __global__ void sum_plane_kernel(long long rows, long long cols, const double2* 
   }
 }
 
+// The same plane in the grouped layout of an A operand: Xs[(i / 8) * 8 cols + j * 8 + i % 8]
+// (rows % 8 == 0): one 8-row group of every column is a contiguous 64-byte run.
+__global__ void sum_plane_grouped_kernel(long long rows, long long cols,
+                                         const double2* __restrict__ X, long long ldx,
+                                         double* __restrict__ Xs) {
+  for (long long j = blockIdx.y; j < cols; j += gridDim.y) {
+    const double2* x = X + j * ldx;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
+         i += (long long)gridDim.x * blockDim.x) {
+      const double2 v = x[i];
+      Xs[(i >> 3) * 8 * cols + j * 8 + (i & 7)] = __dadd_rn(v.x, v.y);
+    }
+  }
+}
+
 __global__ void real_diag_kernel(long long n, const double2* A, long long lda, double* out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -464,6 +479,22 @@ int sum_plane(Handle* h, long long rows, long long cols, const double2* X, long 
   const long long by = std::min<long long>(cols, 65535);
   sum_plane_kernel<<<dim3((unsigned)bx, (unsigned)by), 256, 0, h->stream>>>(rows, cols, X, ldx, Xs,
                                                                            ldxs);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
+int sum_plane_grouped(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
+                      double* Xs) {
+  if (rows * cols <= 0) return OK;
+  if (rows % 8 != 0) {
+    set_error("sum_plane_grouped: rows must be a multiple of 8");
+    return ERR_ARG;
+  }
+  const long long bx = std::min<long long>((rows + 255) / 256, 64);
+  const long long by = std::min<long long>(cols, 65535);
+  sum_plane_grouped_kernel<<<dim3((unsigned)bx, (unsigned)by), 256, 0, h->stream>>>(rows, cols, X,
+                                                                                   ldx, Xs);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;

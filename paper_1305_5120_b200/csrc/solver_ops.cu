@@ -113,9 +113,9 @@ static std::vector<double> filter_coefs(int degree, double a, double b, double l
   return coef;
 }
 
-// 3M operand-sum planes of one filter call (complex_mul() == 3): Hs = Re H + Im H and one
-// plane per rotating block (Y, W), ld rounded up to an even count (TMA strides are
-// multiples of 16 B). Each fused step reads the planes of H and of its input block and
+// 3M operand-sum planes of one filter call (complex_mul() == 3, n % 8 == 0): Hs = Re H +
+// Im H in the grouped A layout and one column-major plane per rotating block (Y, W), ld
+// rounded up to an even count (TMA strides are multiples of 16 B). Each fused step reads the planes of H and of its input block and
 // writes the plane of its output from the epilogue, so no step adds DADDs to the DMMA
 // stream. nullptr when 3M is off or the block is empty.
 struct FilterSums {
@@ -128,7 +128,7 @@ struct FilterSums {
 static int filter_sums(Handle* h, long long n, long long k, const double2* H, long long ldh,
                        const double2* Y, long long ldy, FilterSums* fs) {
   *fs = FilterSums{};
-  if (complex_mul() != 3 || n <= 0 || k <= 0) return OK;
+  if (complex_mul() != 3 || n <= 0 || k <= 0 || n % 8 != 0) return OK;
   const long long ld = (n + 1) & ~1LL;
   fs->ldh = fs->ldy = ld;
   // a declared operator (chfsi_declare_operator) keeps its plane across calls
@@ -138,7 +138,7 @@ static int filter_sums(Handle* h, long long n, long long k, const double2* H, lo
   fs->Ys = (double*)scratch(h, SLOT_YSUM, (size_t)2 * ld * k * sizeof(double));
   if (!fs->Hs || !fs->Ys) return ERR_NOMEM;
   fs->Ws = fs->Ys + ld * k;
-  if (!declared) CHFSI_TRY(sum_plane(h, n, n, H, ldh, fs->Hs, ld));
+  if (!declared) CHFSI_TRY(sum_plane_grouped(h, n, n, H, ldh, fs->Hs));
   return sum_plane(h, n, k, Y, ldy, fs->Ys, ld);
 }
 
@@ -147,7 +147,7 @@ static int filter_sums(Handle* h, long long n, long long k, const double2* H, lo
 int declare_operator(Handle* h, long long n, const double2* H, long long ldh) {
   h->op_ptr = nullptr;
   h->op_n = h->op_ld = 0;
-  if (H == nullptr || n <= 0 || complex_mul() != 3) return OK;
+  if (H == nullptr || n <= 0 || complex_mul() != 3 || n % 8 != 0) return OK;
   if (ldh < n) {
     set_error("declare_operator: ldh must be >= n");
     return ERR_ARG;
@@ -155,7 +155,7 @@ int declare_operator(Handle* h, long long n, const double2* H, long long ldh) {
   const long long ld = (n + 1) & ~1LL;
   double* hs = (double*)scratch(h, SLOT_HSUM, (size_t)ld * n * sizeof(double));
   if (!hs) return ERR_NOMEM;
-  CHFSI_TRY(sum_plane(h, n, n, H, ldh, hs, ld));
+  CHFSI_TRY(sum_plane_grouped(h, n, n, H, ldh, hs));
   h->op_ptr = H;
   h->op_n = n;
   h->op_ld = ldh;

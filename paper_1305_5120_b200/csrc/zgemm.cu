@@ -416,16 +416,62 @@ int encode_real(CUtensorMap* map, const double* base, long long rows, long long 
   return OK;
 }
 
+int encode_3d(CUtensorMap* map, const void* base, const cuuint64_t dims[3],
+              const cuuint64_t strides[2], const cuuint32_t box[3], CUtensorMapSwizzle sw) {
+  auto enc = tensor_map_encoder();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled entry point unavailable");
+    return ERR_CUDA;
+  }
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3-D) failed: " + std::to_string((int)r));
+    return ERR_CUDA;
+  }
+  return OK;
+}
+
+// A (column-major, M % 8 == 0) as one 3-D box per stage {16 doubles of an 8-row
+// group, BK columns (ld * 16 B), BM/8 groups (128 B apart)}, 128-byte swizzle (four TMA
+// issues per stage with sum planes instead of 2 BM/8 + 2: the producer lane's issue
+// code had been ~6 % of warp stall samples).
+int encode_a3d(CUtensorMap* ma, const GemmParams& p, int bm, int bk) {
+  const cuuint64_t G = (cuuint64_t)(p.M / 8);
+  // dims ordered {row-in-group, column, group} so the box lands as [group][col][row]
+  // (the 2-D kernels' layout; the swizzle phase is the column): strides not monotone
+  const cuuint64_t dims[3] = {16, (cuuint64_t)p.K, G};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.lda * 16, 128};
+  const cuuint32_t box[3] = {16, (cuuint32_t)bk, (cuuint32_t)(bm / 8)};
+  return encode_3d(ma, p.A, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Sum-plane kernels: A as above; As in the grouped layout {8 rows, K columns (64 B),
+// M/8 groups}.
+int encode_sums_a(CUtensorMap* ma, CUtensorMap* mas, const GemmParams& p, int bm, int bk) {
+  const cuuint64_t G = (cuuint64_t)(p.M / 8);
+  CHFSI_TRY(encode_a3d(ma, p, bm, bk));
+  const cuuint64_t dims[3] = {8, (cuuint64_t)p.K, G};
+  const cuuint64_t strides[2] = {64, (cuuint64_t)p.K * 64};
+  const cuuint32_t box[3] = {8, (cuuint32_t)bk, (cuuint32_t)(bm / 8)};
+  return encode_3d(mas, p.As, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
 int run_kernel(Handle* h, int c, const Entry& e, dim3 grid, const GemmParams& p) {
   if (!e.tma) {
     e.fn<<<grid, e.threads, e.smem, h->stream>>>(p);
   } else {
     // A: M x K (8-row boxes, BK = 8 columns); B: K x N (BK rows, BN columns)
     CUtensorMap ma, mb, mas, mbs;
-    CHFSI_TRY(encode_colmajor(&ma, p.A, p.M, p.K, p.lda, 8, kBKc[c]));
+    if (p.a3d)
+      CHFSI_TRY(encode_a3d(&ma, p, kBM[c], kBKc[c]));
+    else
+      CHFSI_TRY(encode_colmajor(&ma, p.A, p.M, p.K, p.lda, 8, kBKc[c]));
     CHFSI_TRY(encode_colmajor(&mb, p.B, p.K, p.N, p.ldb, kBKc[c], kBN[c]));
     if (c >= FIRST_SUMS) {
-      CHFSI_TRY(encode_real(&mas, p.As, p.M, p.K, p.ldas, 8, kBKc[c], false));
+      CHFSI_TRY(encode_sums_a(&ma, &mas, p, kBM[c], kBKc[c]));
       CHFSI_TRY(encode_real(&mbs, p.Bs, p.K, p.N, p.ldbs, kBKc[c], kBN[c], true));
     } else {
       mas = ma;
@@ -453,9 +499,10 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.N = (int)N;
   p.K = (int)K;
   const bool sums = p.As != nullptr && p.Bs != nullptr && g_mul == 3 && opa == OP_N &&
-                    opb == OP_N && g_tma_enabled;
+                    opb == OP_N && g_tma_enabled && M % 8 == 0;
   const Plan pl = cached_plan(h, opa, opb, epi, M, N, K, sums);
   const int c = pl.cfg;
+  p.a3d = (M % 8 == 0) ? 1 : 0;  // one 3-D A box per stage (TMA kernels)
   if (c >= FIRST_SUMS && !sums) {
     set_error("zgemm: forced config " + std::to_string(c) + " needs operand sum planes");
     return ERR_ARG;

@@ -51,9 +51,13 @@ struct GemmParams {
   // shard of L^-1 A L^-H multiplies by rows [tri_off, tri_off + N) of L^-1).
   int tri;
   int tri_off;
-  // 3M operand-sum planes (real, column-major; ld in doubles): As = Re A + Im A (M x K),
-  // Bs = Re B + Im B (K x N); Cs (optional, EPI_FILTER / EPI_STORE of the TMA kernels and
-  // the split-K reduce) receives Re C + Im C of the result, the next step's Bs
+  // 3M operand-sum planes: As = Re A + Im A (M x K, M % 8 == 0) in the grouped layout
+  // As[(i / 8) * 8 K + j * 8 + i % 8] (ldas unused); Bs = Re B + Im B (K x N,
+  // column-major, ld in doubles); Cs (optional, EPI_FILTER / EPI_STORE of the TMA kernels
+  // and the split-K reduce) receives Re C + Im C of the result, column-major: the next
+  // step's Bs
+  // TMA kernels: A arrives as one 3-D box per stage (M % 8 == 0), set by the launcher
+  int a3d;
   const double* As; long long ldas;
   const double* Bs; long long ldbs;
   double* Cs; long long ldcs;

@@ -129,6 +129,9 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
       #pragma unroll
       for (int i = 0; i < FM; ++i) {
         const int mg = (wm * WM) / 8 + i;
+        // smem [group][col][8 rows] (one 3-D box or BM/8 2-D boxes): 128-byte row index
+        // mg * BK + kk, swizzle phase kk -- every quarter-warp reads 8 distinct 16-byte
+        // bank groups
         fa[i] = lds128(a + 16u * ((mg * BK + kk) * 8 + (pr ^ kk)));
       }
       #pragma unroll
@@ -141,7 +144,7 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
         // per 3 FM FN DMMAs.
         double as[FM], bs[FN];
         if (SUMS) {
-          // precomputed operand sums: As box g = {8 rows, BK cols} unswizzled (64 B per
+          // precomputed operand sums: As [group][col][8 rows] unswizzled (64 B per group
           // column), Bs = {BK rows, BN cols} with 64-byte swizzle; both conflict-free
           #pragma unroll
           for (int i = 0; i < FM; ++i) {
@@ -281,15 +284,23 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     mbar_expect_tx(&full[s], STAGE_BYTES);
     // A: one {8 rows x BK cols} box per 8-row group (coords in doubles, columns);
     // B: one {BK rows x BN cols} box. Out-of-range rows/cols arrive zero-filled.
-    #pragma unroll
-    for (int g = 0; g < BM / 8; ++g)
-      tma_load_2d(sA + s * A_ELEMS + g * BK * 8, &mapA, 2 * (m0 + 8 * g), k0, &full[s]);
-    tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
     if (SUMS) {
-      #pragma unroll
-      for (int g = 0; g < BM / 8; ++g)
-        tma_load_2d(sAs + s * A_ELEMS + g * BK * 8, &mapAs, m0 + 8 * g, k0, &full[s]);
+      // four boxes per stage: A {16 doubles, BK cols, BM/8 groups} (M % 8 == 0), B, the
+      // grouped A-sum plane {8 rows, BK cols, BM/8 groups} and the B-sum plane
+      tma_load_3d(sA + s * A_ELEMS, &mapA, 0, k0, m0 / 8, &full[s]);
+      tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
+      tma_load_3d(sAs + s * A_ELEMS, &mapAs, 0, k0, m0 / 8, &full[s]);
       tma_load_2d(sBs + s * B_ELEMS, &mapBs, k0, n0, &full[s]);
+    } else {
+      // A: one 3-D box when M % 8 == 0 (p.a3d, same smem layout), else BM/8 2-D boxes
+      if (p.a3d) {
+        tma_load_3d(sA + s * A_ELEMS, &mapA, 0, k0, m0 / 8, &full[s]);
+      } else {
+        #pragma unroll
+        for (int g = 0; g < BM / 8; ++g)
+          tma_load_2d(sA + s * A_ELEMS + g * BK * 8, &mapA, 2 * (m0 + 8 * g), k0, &full[s]);
+      }
+      tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
     }
   };
 
