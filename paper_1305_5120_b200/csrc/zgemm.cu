@@ -538,7 +538,10 @@ int launch_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, 
     return s ? std::max(1, atoi(s)) : 0;
   }();
   int group = 1;
-  if (g_table[c][opa][opb][epi].tma && 16.0 * (double)K * (double)N > 64e6) {
+  // (split-K: the panel of one K chunk; at k = 210, split 8 the full-K test had grouped
+  // anyway and read 56 GB of DRAM per launch instead of 12.7 GB, at equal speed)
+  const double panel_k = pl.split > 1 ? (double)pl.k_chunk : (double)K;
+  if (g_table[c][opa][opb][epi].tma && 16.0 * panel_k * (double)N > 64e6) {
     const long long resident = (long long)g_table[c][opa][opb][epi].occ * h->sm_count;
     group = (int)std::max<long long>(1, resident / std::max(1, p.tiles_n));
   }
