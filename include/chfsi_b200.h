@@ -206,6 +206,12 @@ int chfsi_get_complex_mul(void);
  * while declared, without re-declaring, gives wrong filter results. */
 int chfsi_declare_operator(chfsi_handle_t h, int64_t n, const void* d_H, int64_t ldh);
 
+/* Y = H X for an n x n operator and an n x k block (core.py:318-330 `_rr_raw`'s H Q,
+ * the re-check H V of core.py:532-544). On the declared operator (above) the product
+ * reads H's 3M sum plane; otherwise it is chfsi_zgemm(N, N). */
+int chfsi_apply_operator(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
+                         const void* d_X, int64_t ldx, void* d_Y, int64_t ldy);
+
 /* Microbenchmarks that give the roofline denominators on the box:
  * FP64 tensor-pipe (DMMA) and FP64 FMA-pipe (DFMA) peak, TFLOP/s. */
 int chfsi_peak_dmma(int device, int iters, double* h_tflops);

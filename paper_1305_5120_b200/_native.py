@@ -78,6 +78,8 @@ SIGNATURES = {
     "chfsi_set_complex_mul": (_int, [_int]),
     "chfsi_get_complex_mul": (_int, []),
     "chfsi_declare_operator": (_int, [_c_void_p, _i64, _c_void_p, _i64]),
+    "chfsi_apply_operator": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64,
+                                     _c_void_p, _i64]),
     "chfsi_gemm_plan": (_int, [_c_void_p, _int, _int, _int, _i64, _i64, _i64, _pint, _pint]),
     "chfsi_peak_dmma": (_int, [_int, _int, _pdbl]),
     "chfsi_peak_dfma": (_int, [_int, _int, _pdbl]),

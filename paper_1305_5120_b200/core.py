@@ -632,7 +632,7 @@ class DeviceSolver:
         if self.sharded is not None:
             final_res = self.sharded.residual_check(self.eng, self.hb, vecs, vals, ws.hq[:nev])
         else:
-            self.eng.zgemm("N", "N", n, nev, n, 1.0, self.hb, vecs, 0.0, ws.hq[:nev])
+            self.eng.apply_operator(self.hb, vecs, ws.hq[:nev])
             final_res = self.eng.residual_norms(ws.hq[:nev], vecs, vals)
         _count_products(nev)
         report.t_resid += time.perf_counter() - t0

@@ -451,6 +451,18 @@ int chfsi_declare_operator(chfsi_handle_t h, int64_t n, const void* d_H, int64_t
   return declare_operator(h, n, (const double2*)d_H, ldh);
 }
 
+int chfsi_apply_operator(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,
+                         const void* d_X, int64_t ldx, void* d_Y, int64_t ldy) {
+  H_CHECK(h);
+  if (n < 0 || k < 0 || ldh < std::max<int64_t>(1, n) || ldx < std::max<int64_t>(1, n) ||
+      ldy < std::max<int64_t>(1, n)) {
+    set_error("apply_operator: bad dimensions");
+    return ERR_ARG;
+  }
+  return apply_operator(h, n, k, (const double2*)d_H, ldh, (const double2*)d_X, ldx,
+                        (double2*)d_Y, ldy);
+}
+
 int chfsi_get_complex_mul(void) { return complex_mul(); }
 
 int chfsi_gemm_plan(chfsi_handle_t h, int opa, int opb, int filter_epilogue, int64_t m, int64_t n,

@@ -135,6 +135,14 @@ int sum_plane(Handle* h, long long rows, long long cols, const double2* X, long 
 int sum_plane_grouped(Handle* h, long long rows, long long cols, const double2* X, long long ldx,
                       double* Xs);
 int declare_operator(Handle* h, long long n, const double2* H, long long ldh);
+// C = A B (op N x N) reading 3M sum planes (sp may be null)
+int zgemm_nn_sums(Handle* h, long long M, long long N, long long K, const double2* A, long long lda,
+                  const double2* B, long long ldb, double2* C, long long ldc,
+                  const SumPlanes* sp);
+// Y = H X; with the declared operator H (chfsi_declare_operator) the product reads H's
+// sum plane and a plane of X formed here (3M without in-loop sums)
+int apply_operator(Handle* h, long long n, long long k, const double2* H, long long ldh,
+                   const double2* X, long long ldx, double2* Y, long long ldy);
 int zgemm_filter_step(Handle* h, long long M, long long N, const double2* A, long long lda,
                       const double2* Y1, long long ld1, double alpha, double beta,
                       const double2* Y0, long long ld0, double gamma, double2* C, long long ldc,

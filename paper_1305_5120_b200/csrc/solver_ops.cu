@@ -142,6 +142,21 @@ static int filter_sums(Handle* h, long long n, long long k, const double2* H, lo
   return sum_plane(h, n, k, Y, ldy, fs->Ys, ld);
 }
 
+int apply_operator(Handle* h, long long n, long long k, const double2* H, long long ldh,
+                   const double2* X, long long ldx, double2* Y, long long ldy) {
+  const bool declared = h->op_ptr == (const void*)H && h->op_n == n && h->op_ld == ldh &&
+                        complex_mul() == 3 && n % 8 == 0;
+  if (!declared || k <= 0)
+    return zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, X, ldx, ZERO, Y, ldy);
+  const long long ld = (n + 1) & ~1LL;
+  double* hs = (double*)scratch(h, SLOT_HSUM, (size_t)ld * n * sizeof(double));
+  double* xs = (double*)scratch(h, SLOT_YSUM, (size_t)ld * k * sizeof(double));
+  if (!hs || !xs) return ERR_NOMEM;
+  CHFSI_TRY(sum_plane(h, n, k, X, ldx, xs, ld));
+  SumPlanes sp{hs, ld, xs, ld, nullptr, 0};
+  return zgemm_nn_sums(h, n, k, n, H, ldh, X, ldx, Y, ldy, &sp);
+}
+
 // chfsi_declare_operator: H stays unchanged until the next declaration (or a clear with
 // H = nullptr); its sum plane is computed now and reused by the filter calls on it.
 int declare_operator(Handle* h, long long n, const double2* H, long long ldh) {
@@ -681,7 +696,7 @@ int rayleigh_ritz(Handle* h, long long n, long long k, const double2* H, long lo
   double* w_dev = v;
   double* r_dev = v + k;
   int* info_dev = reinterpret_cast<int*>(v + 2 * k);
-  if (!hq_ready) CHFSI_TRY(zgemm(h, OP_N, OP_N, n, k, n, ONE, H, ldh, Q, ldq, ZERO, HQ, ldhq));
+  if (!hq_ready) CHFSI_TRY(apply_operator(h, n, k, H, ldh, Q, ldq, HQ, ldhq));
   CHFSI_TRY(zgemm(h, OP_C, OP_N, k, k, n, ONE, Q, ldq, HQ, ldhq, ZERO, G, k));
   CHFSI_TRY(hermitize(h, k, G, k));
   CHFSI_TRY(eig_small(h, k, G, k, w_dev, info_dev));

@@ -650,6 +650,23 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
   return launch(h, opa, opb, EPI_STORE, M, N, K, p);
 }
 
+int zgemm_nn_sums(Handle* h, long long M, long long N, long long K, const double2* A, long long lda,
+                  const double2* B, long long ldb, double2* C, long long ldc,
+                  const SumPlanes* sp) {
+  GemmParams p{};
+  p.A = A; p.lda = lda;
+  p.B = B; p.ldb = ldb;
+  p.C = C; p.ldc = ldc;
+  p.alpha = make_double2(1.0, 0.0);
+  p.beta = make_double2(0.0, 0.0);
+  if (sp != nullptr) {
+    p.As = sp->As; p.ldas = sp->ldas;
+    p.Bs = sp->Bs; p.ldbs = sp->ldbs;
+    p.Cs = sp->Cs; p.ldcs = sp->ldcs;
+  }
+  return launch(h, OP_N, OP_N, EPI_STORE, M, N, K, p);
+}
+
 int zgemm_filter_panel(Handle* h, long long M, long long N, long long K, const double2* A,
                        long long lda, const double2* B, long long ldb, const double2* Y1e,
                        long long ld1e, double alpha, double beta, const double2* Y0, long long ld0,

@@ -192,6 +192,13 @@ class Engine:
         else:
             _native.call("chfsi_declare_operator", self.h, rows(H), ptr(H), ld(H))
 
+    def apply_operator(self, H, X, Y):
+        """Y = H X (reads H's 3M sum plane when H is the declared operator)."""
+        n, k = rows(X), cols(X)
+        _native.call("chfsi_apply_operator", self.h, n, k, ptr(H), ld(H), ptr(X), ld(X), ptr(Y),
+                     ld(Y))
+        return Y
+
     def filter_step(self, H, Y1, alpha, beta, Y0, gamma, C):
         n, k = rows(Y1), cols(Y1)
         _native.call("chfsi_filter_step", self.h, n, k, ptr(H), ld(H), ptr(Y1), ld(Y1),

@@ -240,7 +240,7 @@ class ShardedPhases:
         lo, hi = sh.range(self.rank)
         w_ = hi - lo
         if w_:
-            eng.zgemm("N", "N", n, w_, n, 1.0, H, Q[lo:hi], 0.0, HQ[lo:hi])
+            eng.apply_operator(H, Q[lo:hi], HQ[lo:hi])
         self._gather(sh, HQ[lo:hi], HQ)
         W = self._scratch("w", k, k, Q)
         if w_:
@@ -278,7 +278,7 @@ class ShardedPhases:
         sh = ColumnShards(k, self.world)
         lo, hi = sh.range(self.rank)
         if hi > lo:
-            eng.zgemm("N", "N", n, hi - lo, n, 1.0, H, V[lo:hi], 0.0, HV[lo:hi])
+            eng.apply_operator(H, V[lo:hi], HV[lo:hi])
             mine = eng.residual_norms(HV[lo:hi], V[lo:hi], vals[lo:hi])
         else:
             mine = np.empty(0)

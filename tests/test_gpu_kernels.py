@@ -445,6 +445,46 @@ def test_filter_with_sum_planes(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
+def test_declared_operator_filter_and_apply(eng):
+    """chfsi_declare_operator: filter calls and H X products on the declared H reuse its
+    sum plane (same results as undeclared, bit for bit); re-declaring after H changes
+    picks up the new H; clearing returns to per-call planes."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    n, k, m = 512, 40, 5
+    h, lam, _ = baseline_matrix(n, n)
+    rng = np.random.default_rng(9)
+    y = crand(rng, n, k)
+    a, b, lam_ref = float(lam[k]), float(lam[-1]) * 1.05, float(lam[0])
+    dH = D.to_device(h, eng.device)
+
+    def run():
+        f = D.to_host(eng.filter(dH, D.to_device(y, eng.device), D.zeros(n, k, eng.device),
+                                 m, a, b, lam_ref))
+        hy = D.to_host(eng.apply_operator(dH, D.to_device(y, eng.device),
+                                          D.zeros(n, k, eng.device)))
+        return f, hy
+
+    f0, hy0 = run()
+    eng.declare_operator(dH)
+    try:
+        f1, hy1 = run()
+        assert np.array_equal(f0, f1) and np.array_equal(hy0, hy1)
+        ref = O.cheb_filter(h, y, m, a, b, lam_ref)
+        assert np.linalg.norm(f1 - ref) <= 1e-12 * np.linalg.norm(ref)
+        assert np.linalg.norm(hy1 - h @ y) <= 1e-14 * np.linalg.norm(h @ y)
+        h2 = 2.0 * h
+        dH.copy_(D.to_device(h2, eng.device))
+        eng.declare_operator(dH)  # H changed: declare again
+        _, hy2 = run()
+        assert np.linalg.norm(hy2 - h2 @ y) <= 1e-14 * np.linalg.norm(h2 @ y)
+    finally:
+        eng.declare_operator(None)
+    _, hy3 = run()
+    assert np.array_equal(hy3, hy2)
+
+
 def test_sum_config_needs_planes(eng):
     """Forcing a sum-reading config on a product without planes is an argument error."""
     from paper_1305_5120_b200 import _native, device as D
