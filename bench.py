@@ -13,7 +13,9 @@ Also reported: e2e (the same filter through the drop-in Python API
 ``chebyshev_filter(H, Y, spec)`` with pinned host H/Y, host<->device copies
 inside the timed region), roofline of the dominant kernel (measured FP64
 tensor-pipe peak), GPU clocks during the timed region, the oracle CPU filter
-on the host cores (cpu_baseline), tail-width throughput and a full c0 solve.
+on the host cores (cpu_baseline), tail-width throughput, a full c0 solve and
+c1 sequence, and at every N the s per ChFSI solve at n = 20000 (solve_c4:
+BASELINE c4 problem 1, column-sharded over the ranks for N > 1).
 
 ``--impl reference`` times the reference algorithm's CPU filter (the oracle
 restatement, numpy/OpenBLAS on all host cores) on a bounded column sample of
@@ -295,8 +297,28 @@ def run_b200(args, rank, world, local_rank):
         # every rank takes part (collectives inside); max over ranks
         e2e_multi = e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up,
                                     lam_ref, dev)
-    if rank != 0:
+    line = None
+    if rank == 0:
+        line = headline_line(args, world, value, ms_per_step, mul, launches, clocks, achieved,
+                             achieved_conv, kernel_name, n, kp, local_rank, t_gen)
+        if e2e_multi is not None:
+            line["e2e"] = e2e_multi
+    if world > 1:
+        if not args.no_extras:
+            # s per ChFSI solve at the metric's n on all ranks (column-sharded)
+            nev_s = int(round(k * 2000 / 2200))
+            solve = guarded_leg(line, rank, lambda: solve_c4_leg(H, lam, rank, world, dev,
+                                                                 nev_s, k - nev_s, m))
+            if rank == 0:
+                line["solve_c4"] = solve
+        if rank == 0:
+            print(json.dumps(line), flush=True)
         return
+    finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, lam_ref, dev, n, m)
+
+
+def headline_line(args, world, value, ms_per_step, mul, launches, clocks, achieved, achieved_conv,
+                  kernel_name, n, kp, local_rank, t_gen):
     peaks = measured_fp64_peaks(local_rank)
     peak = peaks["dmma_tflops"]
     traffic = committed_traffic(n, kp)
@@ -321,9 +343,12 @@ def run_b200(args, rank, world, local_rank):
                      "peaks": peaks},
         "setup_s": t_gen,
     }
-    if e2e_multi is not None:
-        line["e2e"] = e2e_multi
-    if world == 1 and not args.no_extras:
+    return line
+
+
+def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, lam_ref, dev, n, m):
+    import torch
+    if not args.no_extras:
         def leg(key, fn):
             # an optional leg must never cost the headline line
             try:
@@ -334,11 +359,15 @@ def run_b200(args, rank, world, local_rank):
 
         leg("e2e", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev))
         leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
-        del H, Yfull, Y0, Y, W
+        del Yfull, Y0, Y, W
+        torch.cuda.empty_cache()
+        nev_s = int(round(args.k * 2000 / 2200))
+        line["solve_c4"] = guarded_leg(line, 0, lambda: solve_c4_leg(
+            H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree))
+        del H
         torch.cuda.empty_cache()
         leg("solve_c0", solve_c0)
         leg("sequence_c1", sequence_c1)
-        leg("c4_outer_iteration", c4_iteration_window)
         leg("generalized_c4_setup", generalized_c4_setup)
 
         def cpu_leg():
@@ -368,6 +397,72 @@ KERNELS = {
 }
 
 
+SOLVE_LEG_LIMIT_S = 900.0
+
+
+def guarded_leg(line, rank, fn, limit_s=SOLVE_LEG_LIMIT_S):
+    """Run a leg that has collectives inside on every rank. An exception is reported in
+    the line; a leg still running after limit_s (e.g. a rank stuck in a collective
+    after another rank failed) makes rank 0 print the headline line with the error and
+    every rank exit 0, so the headline is never lost."""
+    import threading
+
+    def fire():
+        if rank == 0 and line is not None:
+            line["solve_c4"] = {"error": f"leg exceeded {limit_s:.0f} s; abandoned"}
+            print(json.dumps(line), flush=True)
+        os._exit(0)
+
+    timer = threading.Timer(limit_s, fire)
+    timer.daemon = True
+    timer.start()
+    try:
+        return fn()
+    except Exception as exc:  # pragma: no cover - reported, not raised
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    finally:
+        timer.cancel()
+
+
+def solve_c4_leg(H, lam, rank, world, dev, nev=2000, nex=200, degree=25):
+    """s per ChFSI solve at the metric's n = 20000 (BASELINE c4 problem 1 in standard
+    form: the c0 spectrum recipe, nev = 2000, nex = 200, m = 25, random start, solver
+    seed 1, opt-in block_top interval; other --matrix-order/--block-cols scale nev/nex)
+    on every rank; for N > 1 column-sharded over the process group with H
+    broadcast from rank 0 (the replicated k x k decisions need the identical operator).
+    Time = max over ranks of the solve's wall time between barriers."""
+    import torch
+    import torch.distributed as dist
+    import paper_1305_5120_b200 as G
+    n = H.shape[0]
+    if world > 1:
+        dist.broadcast(H, src=0)
+    hm = G.HermitianDenseMatrix.from_device(H, trusted=True)
+    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=degree, max_outer_iters=2000,
+                         interval="block_top")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    vals, vecs, rep = G.chfsi_solve(hm, None, cfg, seed=1,
+                                    group=dist.group.WORLD if world > 1 else None)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt, rep.t_filter], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    dt, tf = float(tt[0]), float(tt[1])
+    flops = 8.0 * n * n * degree * sum(it.filtered_cols for it in rep.iterations)
+    del vecs
+    return {"n": n, "nev": nev, "nex": nex, "degree": degree, "interval": "block_top",
+            "n_gpus": world, "s_per_solve": dt, "outer_iterations": rep.outer_iterations,
+            "total_matmuls": rep.total_matmuls,
+            "filter_tflops_whole_job": flops / tf / 1e12 if tf > 0 else None,
+            "filter_share": tf / dt,
+            "residuals_below_tol": bool(rep.converged),
+            "max_rel_eig_err_vs_exact": float(np.max(np.abs(vals - lam[:nev]) / np.abs(lam[:nev])))}
+
+
 def plan_kernel_name(eng, n, k):
     import ctypes
     from paper_1305_5120_b200 import _native
@@ -376,33 +471,6 @@ def plan_kernel_name(eng, n, k):
     _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg), ctypes.byref(split))
     name = KERNELS.get(cfg.value, f"cfg{cfg.value}")
     return name + (f" split-K {split.value}" if split.value > 1 else "")
-
-
-def c4_iteration_window(n=20000, nev=2000, nex=200, degree=25):
-    """One full-width ChFSI outer iteration at c4 shape (bootstrap RR + iteration 1),
-    phase times from the solver's own report (max_outer_iters=1 -> NotConverged)."""
-    import paper_1305_5120_b200 as G
-    import torch
-    from paper_1305_5120_b200 import workloads as Wl
-    H, lam = Wl.spectrum_matrix_torch(0, n, torch.device("cuda", torch.cuda.current_device()))
-    hm = G.HermitianDenseMatrix.from_device(H, trusted=True)
-    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=degree, max_outer_iters=1)
-    t0 = time.perf_counter()
-    try:
-        G.chfsi_solve(hm, None, cfg, seed=1)
-        rep = None
-    except G.NotConverged as exc:
-        rep = exc.report
-    dt = time.perf_counter() - t0
-    if rep is None:
-        return {"error": "converged in one iteration (unexpected)"}
-    it = rep.iterations[0]
-    return {"n": n, "k": nev + nex, "degree": degree, "wall_s": dt,
-            "t_lanczos": rep.t_lanczos, "t_bootstrap_rr": rep.t_rr - it.t_rr,
-            "iteration": {"t_filter": it.t_filter, "t_qr": it.t_qr, "t_rr": it.t_rr,
-                          "t_resid": it.t_resid, "filtered_cols": it.filtered_cols,
-                          "locked": it.converged},
-            "filter_share_of_iteration": it.t_filter / (it.t_filter + it.t_qr + it.t_rr + it.t_resid)}
 
 
 def generalized_c4_setup(n=20000):

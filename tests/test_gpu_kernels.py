@@ -447,8 +447,9 @@ def test_filter_with_sum_planes(eng, cfg, split):
 
 def test_declared_operator_filter_and_apply(eng):
     """chfsi_declare_operator: filter calls and H X products on the declared H reuse its
-    sum plane (same results as undeclared, bit for bit); re-declaring after H changes
-    picks up the new H; clearing returns to per-call planes."""
+    sum plane (filter: the same result as undeclared, bit for bit; H X: the plan may
+    differ in split-K, so to rounding); re-declaring after H changes picks up the new H;
+    clearing returns to per-call planes."""
     import oracle.chfsi_oracle as O
     from paper_1305_5120_b200 import device as D
     from paper_1305_5120_b200.workloads import baseline_matrix
@@ -470,7 +471,8 @@ def test_declared_operator_filter_and_apply(eng):
     eng.declare_operator(dH)
     try:
         f1, hy1 = run()
-        assert np.array_equal(f0, f1) and np.array_equal(hy0, hy1)
+        assert np.array_equal(f0, f1)
+        assert np.linalg.norm(hy1 - hy0) <= 1e-15 * np.linalg.norm(hy0) * n ** 0.5
         ref = O.cheb_filter(h, y, m, a, b, lam_ref)
         assert np.linalg.norm(f1 - ref) <= 1e-12 * np.linalg.norm(ref)
         assert np.linalg.norm(hy1 - h @ y) <= 1e-14 * np.linalg.norm(h @ y)
@@ -482,7 +484,7 @@ def test_declared_operator_filter_and_apply(eng):
     finally:
         eng.declare_operator(None)
     _, hy3 = run()
-    assert np.array_equal(hy3, hy2)
+    assert np.linalg.norm(hy3 - hy2) <= 1e-15 * np.linalg.norm(hy2) * n ** 0.5
 
 
 def test_sum_config_needs_planes(eng):
