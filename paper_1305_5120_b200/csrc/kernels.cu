@@ -289,8 +289,11 @@ __global__ void sum_plane_kernel(long long rows, long long cols, const double2* 
   }
 }
 
-// The same plane in the grouped layout of an A operand: Xs[(i / 8) * 8 cols + j * 8 + i % 8]
-// (rows % 8 == 0): one 8-row group of every column is a contiguous 64-byte run.
+// The same plane in the grouped layout of an A operand (rows % 8 == 0): one 8-row group
+// of every column is a contiguous 64-byte run, Xs[(i / 8) * 8 cols + j * 8 + p], with the
+// row position p = (i % 8) ^ (2 * ((j / 2) % 2)) so that the fragment reads of a half-warp
+// (4 rows x 4 columns) fall in 16 distinct 8-byte bank pairs (unpermuted, columns j and
+// j + 2 collide: 2-way conflicts).
 __global__ void sum_plane_grouped_kernel(long long rows, long long cols,
                                          const double2* __restrict__ X, long long ldx,
                                          double* __restrict__ Xs) {
@@ -299,7 +302,7 @@ __global__ void sum_plane_grouped_kernel(long long rows, long long cols,
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < rows;
          i += (long long)gridDim.x * blockDim.x) {
       const double2 v = x[i];
-      Xs[(i >> 3) * 8 * cols + j * 8 + (i & 7)] = __dadd_rn(v.x, v.y);
+      Xs[(i >> 3) * 8 * cols + j * 8 + ((i & 7) ^ (((j >> 1) & 1) << 1))] = __dadd_rn(v.x, v.y);
     }
   }
 }

@@ -52,7 +52,7 @@ struct GemmParams {
   int tri;
   int tri_off;
   // 3M operand-sum planes: As = Re A + Im A (M x K, M % 8 == 0) in the grouped layout
-  // As[(i / 8) * 8 K + j * 8 + i % 8] (ldas unused); Bs = Re B + Im B (K x N,
+  // As[(i / 8) * 8 K + j * 8 + ((i % 8) ^ (2 * ((j / 2) % 2)))] (ldas unused); Bs = Re B + Im B (K x N,
   // column-major, ld in doubles); Cs (optional, EPI_FILTER / EPI_STORE of the TMA kernels
   // and the split-K reduce) receives Re C + Im C of the result, column-major: the next
   // step's Bs

@@ -144,12 +144,13 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
         // per 3 FM FN DMMAs.
         double as[FM], bs[FN];
         if (SUMS) {
-          // precomputed operand sums: As [group][col][8 rows] unswizzled (64 B per group
-          // column), Bs = {BK rows, BN cols} with 64-byte swizzle; both conflict-free
+          // precomputed operand sums: As [group][col][8 rows] (64 B per group column,
+          // rows permuted by column: sum_plane_grouped), Bs = {BK rows, BN cols} with
+          // 64-byte swizzle; both conflict-free per half-warp
           #pragma unroll
           for (int i = 0; i < FM; ++i) {
             const int mg = (wm * WM) / 8 + i;
-            as[i] = lds64(as_base + 8u * (mg * 64 + kk * 8 + pr));
+            as[i] = lds64(as_base + 8u * (mg * 64 + kk * 8 + (pr ^ (((kk >> 1) & 1) << 1))));
           }
           #pragma unroll
           for (int j = 0; j < FN; ++j) {
