@@ -27,3 +27,29 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["n"] == 600 and "non-default" in d["metric"]
+
+
+def test_guarded_leg_reports_errors_and_abandons_a_stuck_leg():
+    """bench.guarded_leg: an exception becomes the leg's error entry; a leg still running
+    at the limit makes rank 0 print the headline line (with the error) and exit 0, so a
+    rank stuck in a collective never costs the headline."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    def boom():
+        raise RuntimeError("collective failed")
+
+    out = bench.guarded_leg({"value": 1.0}, 0, boom, limit_s=30.0)
+    assert out == {"error": "RuntimeError: collective failed"}
+    assert bench.guarded_leg(None, 1, lambda: {"s_per_solve": 1.0}, limit_s=30.0) == \
+        {"s_per_solve": 1.0}
+    code = ("import sys, time; sys.path.insert(0, %r); import bench; "
+            "bench.guarded_leg({'metric': 'm', 'value': 2.0}, 0, lambda: time.sleep(60), "
+            "limit_s=1.0); print('not reached')" % ROOT)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=120, cwd=ROOT)
+    assert res.returncode == 0
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and "not reached" not in res.stdout
+    d = json.loads(lines[0])
+    assert d["value"] == 2.0 and "abandoned" in d["solve_c4"]["error"]
