@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--degree", type=int, default=25)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/tail/solve legs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--complex-mul", type=int, default=3, choices=[3, 4],
+                    help="complex products of the GEMMs: 3 (3M, default) or 4 real DMMA "
+                         "products (the north star's literal four-MMA form)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: host-staged, for testing)")
     return ap.parse_args()
@@ -209,6 +212,7 @@ def run_b200(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     eng = D.Engine.get(dev)
+    eng.set_complex_mul(args.complex_mul)
     n, k, m = args.n, args.k, args.degree
 
     # ---- data: H (c0 spectrum recipe, seeded) replicated on every rank
@@ -359,6 +363,9 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
 
         leg("e2e", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev))
         leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
+        other = 4 if args.complex_mul == 3 else 3
+        leg(f"filter_complex_mul_{other}",
+            lambda: filter_other_mul(eng, H, Y0, Y, W, m, a_edge, b_up, lam_ref, other))
         del Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         nev_s = int(round(args.k * 2000 / 2200))
@@ -621,6 +628,33 @@ def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
             "h2d_bytes_per_step": int(16 * n * n + 16 * n * k),
             "d2h_bytes_per_step": int(res.nbytes), "steps": steps,
             "path": "paper_1305_5120_b200.chebyshev_filter(H, Y, FilterSpec) -> VectorBlock.entries"}
+
+
+def filter_other_mul(eng, H, Y0, Y, W, degree, a_edge, b_up, lam_ref, mul, steps=2):
+    """The headline filter call with the other complex-product scheme (the north star's
+    literal four real MMAs when the headline runs 3M), timed the same way; restores the
+    headline scheme afterwards."""
+    import torch
+    n, k = H.shape[0], Y0.shape[0]
+    old = eng.complex_mul()
+    eng.set_complex_mul(mul)
+    try:
+        Y.copy_(Y0)
+        eng.filter(H, Y, W, degree, a_edge, b_up, lam_ref)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(steps):
+            Y.copy_(Y0)
+            eng.filter(H, Y, W, degree, a_edge, b_up, lam_ref)
+        b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e-3 / steps
+    finally:
+        eng.set_complex_mul(old)
+    return {"complex_mul": mul, "value": 8.0 * n * n * k * degree / t / 1e12, "unit": UNIT,
+            "ms_per_step": t * 1e3, "steps": steps,
+            "executed_dmma_tflops": 2.0 * mul * n * n * k * degree / t / 1e12}
 
 
 def tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref, degree=5):

@@ -87,7 +87,7 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 16;
+constexpr int NCFG = 17;
 constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
 constexpr int FIRST_3M = 11;  // cfgs >= 11: the TMA kernels with 3M complex products
 constexpr int FIRST_SUMS = 14;  // cfgs >= 14: 3M reading precomputed operand-sum planes
@@ -129,10 +129,14 @@ using T13 = TmaT<64, 32, 16, 16, 4, 2, 3>;
 // cfg 14 / 15: cfg 11 / 12 reading precomputed operand-sum planes (3M without in-loop DADDs)
 using T14 = TmaT<64, 32, 32, 16, 4, 3, 3, true>;
 using T15 = TmaT<64, 32, 16, 32, 4, 3, 3, true>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64, 64, 64};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32, 32, 32};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8};
-const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16, 16, 32};  // warp tile width
+// cfg 16: sum planes, 64x24 tile of four 16x24 warps stacked by rows: 24-column tiles
+// fit block widths that 32-column tiles round up badly (a 550-column shard: 23 x 24 =
+// 552 vs 18 x 32 = 576 columns of work)
+using T16 = TmaT<64, 24, 16, 24, 4, 3, 3, true>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32, 32, 32, 24};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8};
+const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16, 16, 32, 24};  // warp tile width
 bool g_tma_enabled = true;
 // complex products in the TMA kernels: 3 (3M, default) or 4 real DMMA products
 int g_mul = [] {
@@ -197,6 +201,7 @@ int ensure_table() {
   put_tma<T13>(13);
   put_tma<T14>(14);
   put_tma<T15>(15);
+  put_tma<T16>(16);
   for (int c = 0; c < NCFG; ++c)
     for (int a = 0; a < 2; ++a)
       for (int b = 0; b < 2; ++b)
@@ -239,7 +244,7 @@ struct Plan {
 //     warps (ncu: DMMA pipe 92.5 % vs 95.7 % active at k = 210): x (1 + kRag / tiles_n);
 //   * split-K adds the reduce pass: kTred + (s + 3) M N 16 B at HBM speed.
 constexpr double kEffNN[NCFG] = {0.906, 0.898, 0.837, 0.823, 0.911, 0.926, 0.885,
-                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13, 1.27, 1.26};
+                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13, 1.27, 1.26, 1.24};
 constexpr double kEffCN[7] = {0.886, 0.927, 0.877, 0.854, 1.058, 0.971, 0.887};
 constexpr double kR0Warps4 = 1.289, kR0Warps8 = 1.108;
 constexpr double kRag = 0.122, kFloor = 0.859;

@@ -375,7 +375,7 @@ def test_trtri_blocked_matches_inverse(eng):
 
 
 # every tile configuration and split factor the cost model can pick, on ragged shapes
-_NCFG = 16
+_NCFG = 17
 _TMA_FIRST = 7
 _SUMS_FIRST = 14  # 3M kernels reading operand-sum planes: filter calls only
 
@@ -414,7 +414,7 @@ def test_every_gemm_config_and_split(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
-@pytest.mark.parametrize("cfg", [-1, _SUMS_FIRST, _SUMS_FIRST + 1, 7, 11])
+@pytest.mark.parametrize("cfg", [-1, _SUMS_FIRST, _SUMS_FIRST + 1, _SUMS_FIRST + 2, 7, 11])
 @pytest.mark.parametrize("split", [0, 1, 3])
 def test_filter_with_sum_planes(eng, cfg, split):
     """chfsi_filter with 3M operand-sum planes (Hs, and per block the plane its step's
