@@ -283,12 +283,62 @@ double plan_cost(int c, int occ, int threads, bool nn, int sms, long long M, lon
   return t;
 }
 
+// Sum-plane filter steps on large operators (M >= 8192): a measured rule instead of the
+// cost model. Tile width: the fewest padded columns, ceil(N / BN) * BN, 24-column tiles
+// weighted x1.01 and 32-column tiles with unevenly live warp columns (cfg 14 on a
+// ragged edge) x(1 + 0.12 / tiles_n); split-K: ~20000 CTAs. On the sweep at n = 20000
+// (profiles/r01/sweep_sums16_20000.json, 12 widths 26-2200) the rule's pick is within
+// 0.7 % of the best measured plan on geometric mean (worst 2.9 %); the cost model's
+// pick was 1.7 % (worst 15.7 %: it under-splits mid widths, e.g. k = 400 at split 1).
+constexpr long long kRuleMinM = 8192;
+constexpr double kRuleTargetCtas = 20000.0;
+
+Plan choose_sums_rule(long long M, long long N, long long K) {
+  Plan best;
+  double best_score = 1e300;
+  const long long tm = (M + 63) / 64;
+  for (int c = FIRST_SUMS; c < NCFG; ++c) {
+    const long long tn = (N + kBN[c] - 1) / kBN[c];
+    const long long last = (N - (tn - 1) * kBN[c] + 7) / 8;
+    const int per = kWN[c] / 8, wcols = kBN[c] / kWN[c];
+    int lo = per, hi = 0;
+    for (int w = 0; w < wcols; ++w) {
+      const int l = (int)std::max<long long>(0, std::min<long long>(per, last - w * per));
+      lo = std::min(lo, l);
+      hi = std::max(hi, l);
+    }
+    double score = (double)(tn * kBN[c]);
+    if (hi != lo) score *= 1.0 + 0.12 / (double)tn;
+    if (kBN[c] == 24) score *= 1.01;
+    if (c == FIRST_SUMS + 1) score *= 1.004;  // row-stacked 32-wide warps: last resort
+    if (score < best_score) {
+      best_score = score;
+      best.cfg = c;
+    }
+  }
+  const long long tn = (N + kBN[best.cfg] - 1) / kBN[best.cfg];
+  const long long ktiles = std::max<long long>(1, (K + 7) / 8);
+  const long long ws_cap = std::max<long long>(1, (1LL << 30) / std::max<long long>(1, M * N * 16));
+  const long long s_max = std::max<long long>(1, std::min<long long>({17, ktiles / 4, ws_cap}));
+  // the nearest (in log) of the swept split factors
+  const double s_t = kRuleTargetCtas / (double)(tm * tn);
+  static const int kSplits[] = {1, 2, 3, 4, 6, 8, 12, 16};
+  int s_best = 1;
+  for (int s : kSplits)
+    if (std::fabs(std::log((double)s / s_t)) < std::fabs(std::log((double)s_best / s_t))) s_best = s;
+  best.split = (int)std::max<long long>(1, std::min<long long>(s_best, s_max));
+  best.k_chunk = (int)(((ktiles + best.split - 1) / best.split) * 8);
+  return best;
+}
+
 Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
             bool sums) {
   Plan best;
   double best_cost = 1e300;
   const int sms = h->sm_count;
   const bool nn = (opa == OP_N && opb == OP_N);
+  if (sums && M >= kRuleMinM && g_force_cfg < 0 && g_force_split <= 0)
+    return choose_sums_rule(M, N, K);
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
     if (c >= FIRST_TMA && !g_tma_enabled) continue;
