@@ -114,12 +114,13 @@ struct TmaT {
   template <int EPI>
   static TmaFn fn() { return &zgemm_tma_kernel<BM, BN, WM, WN, ST, EPI, MINB, MUL, SUMS>; }
 };
-// (explicit min-blocks keep ptxas at <= 128 regs -> 4 CTAs / SM for the 64x32 tile;
-// a register-double-buffered fragment variant measured 1.5-2 % slower, profiles/r01)
-using T7 = TmaT<64, 32, 32, 16, 4, 4>;
+// (four-product TMA kernels: 3 CTAs / SM -- the unrolled main loop spills at 128 registers;
+// 3 vs 4 CTAs / SM measured equal before the unroll. A register-double-buffered fragment
+// variant measured 1.5-2 % slower, profiles/r01)
+using T7 = TmaT<64, 32, 32, 16, 4, 3>;
 using T8 = TmaT<64, 16, 16, 16, 4, 4>;
 using T9 = TmaT<64, 64, 32, 32, 4, 2>;
-using T10 = TmaT<64, 32, 16, 32, 4, 4>;
+using T10 = TmaT<64, 32, 16, 32, 4, 3>;
 // cfg 11 / 12: cfg 7 / cfg 10 with 3M complex products (three real DMMA products per
 // complex MAC; 48 accumulator doubles per thread -> 3 CTAs / SM)
 using T11 = TmaT<64, 32, 32, 16, 4, 3, 3>;

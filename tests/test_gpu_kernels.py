@@ -445,6 +445,43 @@ def test_filter_with_sum_planes(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
+def test_filter_width_rule_large_operator(eng):
+    """Operators of order >= 8192 plan their sum-plane filter steps by the width rule
+    (24- or 32-column tiles, split-K to ~20000 CTAs): ragged and tiny widths against a
+    torch (cuBLAS ZGEMM) product step by step, and the rule's plans are the ones used."""
+    import ctypes
+    import torch
+    from paper_1305_5120_b200 import _native
+    n = 8192
+    dev = eng.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    H = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+    H = (H + H.mH) * 0.5
+    H = H.contiguous()
+    eng.declare_operator(H)
+    try:
+        for k in (1, 8, 26, 40, 100, 550):
+            cfg, split = ctypes.c_int(), ctypes.c_int()
+            _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg),
+                         ctypes.byref(split))
+            assert cfg.value >= _SUMS_FIRST, (k, cfg.value)
+            Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
+            W = torch.empty_like(Y)
+            a, b, lam_ref = -1.0, 1.0, -2.0
+            # degree-2 filter: Y1 = s1/e (H - c) Y, Y2 = 2 s2/e (H - c) Y1 - s1 s2 Y
+            c, e = (a + b) / 2, (b - a) / 2
+            s1 = e / (lam_ref - c)
+            s2 = 1.0 / (2.0 / s1 - s1)
+            ref1 = (s1 / e) * (Y @ H - c * Y)  # (k, n) rows are columns: (H Y)^T = Y^T H^T
+            ref2 = (2 * s2 / e) * (ref1 @ H - c * ref1) - s1 * s2 * Y
+            out = eng.filter(H, Y.clone(), W, 2, a, b, lam_ref)
+            err = float(torch.linalg.norm(out - ref2) / torch.linalg.norm(ref2))
+            assert err <= 1e-13, (k, err)
+    finally:
+        eng.declare_operator(None)
+
+
 def test_declared_operator_filter_and_apply(eng):
     """chfsi_declare_operator: filter calls and H X products on the declared H reuse its
     sum plane (filter: the same result as undeclared, bit for bit; H X: the plan may
