@@ -482,6 +482,43 @@ def test_filter_width_rule_large_operator(eng):
         eng.declare_operator(None)
 
 
+@pytest.mark.parametrize("declared", [False, True])
+def test_filter_sum_planes_with_padded_leading_dims(eng, declared):
+    """Sum-plane filter steps on views with ld > n (H, Y and W inside larger buffers):
+    the 3-D A box, the grouped H plane and the block planes honour the leading dims."""
+    import torch
+    n, k, pad = 1024, 50, 24
+    dev = eng.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    Hbuf = torch.randn((n, n + pad), dtype=torch.complex128, device=dev, generator=g)
+    H = Hbuf[:, :n]
+    Hd = H.contiguous()
+    Hd = (Hd + Hd.mH) * 0.5
+    H.copy_(Hd)
+    Ybuf = torch.randn((k, n + pad), dtype=torch.complex128, device=dev, generator=g)
+    Y = Ybuf[:, :n]
+    Wbuf = torch.zeros((k, n + 2 * pad), dtype=torch.complex128, device=dev)
+    W = Wbuf[:, pad:pad + n]
+    a, b, lam_ref = -1.0, 1.0, -2.0
+    c, e = (a + b) / 2, (b - a) / 2
+    s1 = e / (lam_ref - c)
+    s2 = 1.0 / (2.0 / s1 - s1)
+    Y0 = Y.clone()
+    ref1 = (s1 / e) * (Y0 @ Hd - c * Y0)
+    ref2 = (2 * s2 / e) * (ref1 @ Hd - c * ref1) - s1 * s2 * Y0
+    if declared:
+        eng.declare_operator(H)
+    try:
+        out = eng.filter(H, Y, W, 2, a, b, lam_ref)
+    finally:
+        if declared:
+            eng.declare_operator(None)
+    err = float(torch.linalg.norm(out - ref2) / torch.linalg.norm(ref2))
+    assert err <= 1e-13, err
+    assert torch.count_nonzero(Wbuf[:, :pad]) == 0 and torch.count_nonzero(Wbuf[:, pad + n:]) == 0
+
+
 def test_declared_operator_filter_and_apply(eng):
     """chfsi_declare_operator: filter calls and H X products on the declared H reuse its
     sum plane (filter: the same result as undeclared, bit for bit; H X: the plan may
