@@ -1,6 +1,8 @@
 """Small end-to-end workload for `compute-sanitizer --tool memcheck`: every GEMM
-config/split on ragged shapes (TMA zero-fill edges), the fused filter, CholQR2 with
-locked vectors, Rayleigh-Ritz, a small solve and a generalized solve."""
+config/split on ragged shapes (TMA zero-fill edges), the 3M sum-plane filter configs
+(forced, every split, ragged widths, padded leading dims, declared operator, the width
+rule at n = 8192), the fused filter, CholQR2 with locked vectors, Rayleigh-Ritz, a small
+solve and a generalized solve."""
 import sys
 
 import numpy as np
@@ -19,7 +21,7 @@ def crand(*s):
     return rng.standard_normal(s) + 1j * rng.standard_normal(s)
 
 
-for cfg in range(11):
+for cfg in range(14):
     for split in (1, 2):
         lib.chfsi_gemm_override(cfg, split)
         for (m, n, k) in [(13, 5, 27), (70, 33, 9)]:
@@ -31,6 +33,32 @@ for cfg in range(11):
                 eng.zgemm(opa, opb, m, n, k, 1.0, D.to_device(A, eng.device),
                           D.to_device(B, eng.device), 0.5, C)
 lib.chfsi_gemm_override(-1, 0)
+# sum-plane filter configs (n % 8 == 0), ragged widths, forced splits
+for cfg in (14, 15, 16, -1):
+    for split in (1, 3, 0):
+        lib.chfsi_gemm_override(cfg, split)
+        for (n, k) in [(136, 5), (64, 37), (200, 26)]:
+            hh = crand(n, n)
+            hh = (hh + hh.conj().T) / 2
+            dH = D.to_device(hh, eng.device)
+            eng.filter(dH, D.to_device(crand(n, k), eng.device), D.zeros(n, k, eng.device), 3,
+                       -1.0, 1.0, -2.0)
+lib.chfsi_gemm_override(-1, 0)
+# padded leading dims + declared operator + apply_operator
+Hbuf = torch.randn((96, 120), dtype=torch.complex128, device=eng.device)
+Hv = Hbuf[:, :96]
+Ybuf = torch.randn((20, 104), dtype=torch.complex128, device=eng.device)
+eng.declare_operator(Hv)
+eng.filter(Hv, Ybuf[:, :96], torch.empty((20, 96), dtype=torch.complex128, device=eng.device),
+           4, -1.0, 1.0, -2.0)
+eng.apply_operator(Hv, Ybuf[:, :96], torch.empty((20, 96), dtype=torch.complex128,
+                                                  device=eng.device))
+eng.declare_operator(None)
+# the width rule (M >= 8192) on a narrow block
+Hbig = torch.randn((8192, 8192), dtype=torch.complex128, device=eng.device)
+eng.filter(Hbig, torch.randn((26, 8192), dtype=torch.complex128, device=eng.device),
+           torch.empty((26, 8192), dtype=torch.complex128, device=eng.device), 2, -1.0, 1.0, -2.0)
+del Hbig
 from paper_1305_5120_b200.workloads import baseline_matrix  # noqa: E402
 h, lam, _ = baseline_matrix(1, 120)
 lam_g, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=10, buffer=6, degree=12,
