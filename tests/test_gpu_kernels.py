@@ -617,6 +617,34 @@ def test_complex_product_scheme(eng, mul):
         lib.chfsi_set_complex_mul(old)
 
 
+def test_full_size_3m_matches_four_products(eng):
+    """At the BASELINE c4 order (n = 20000) a filter call with 3M sum-plane kernels and
+    one with four-product kernels agree to rounding on a 40-column block (the width
+    rule's pick vs the cost model's four-product pick)."""
+    import torch
+    from paper_1305_5120_b200 import _native
+    lib = _native.load()
+    n, k, m = 20000, 40, 3
+    dev = eng.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    H = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+    H = (H + H.mH) * 0.5
+    Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
+    old = lib.chfsi_get_complex_mul()
+    outs = []
+    try:
+        for mul in (3, 4):
+            assert lib.chfsi_set_complex_mul(mul) == 0
+            W = torch.empty_like(Y)
+            outs.append(eng.filter(H, Y.clone(), W, m, -1.0, 1.0, -2.0).clone())
+    finally:
+        lib.chfsi_set_complex_mul(old)
+    del H
+    err = float(torch.linalg.norm(outs[0] - outs[1]) / torch.linalg.norm(outs[1]))
+    assert err <= 1e-13, err
+
+
 def test_full_size_filter_on_exact_eigenvectors(eng):
     """Size-independent property at BASELINE c4 size (n = 20000): for an exact
     eigenvector q_j of H, p_m(H) q_j = p_m(lambda_j) q_j with the scalar closed form."""
