@@ -291,7 +291,13 @@ double plan_cost(int c, int occ, int threads, bool nn, int sms, long long M, lon
 // (profiles/r01/sweep_sums16_20000.json, 12 widths 26-2200) the rule's pick is within
 // 0.7 % of the best measured plan on geometric mean (worst 2.9 %); the cost model's
 // pick was 1.7 % (worst 15.7 %: it under-splits mid widths, e.g. k = 400 at split 1).
-constexpr long long kRuleMinM = 8192;
+long long rule_min_m() {
+  static const long long v = [] {
+    const char* e = getenv("CHFSI_RULE_MIN_M");  // tuning only
+    return e ? atoll(e) : 8192LL;
+  }();
+  return v;
+}
 constexpr double kRuleTargetCtas = 20000.0;
 
 Plan choose_sums_rule(long long M, long long N, long long K) {
@@ -338,7 +344,7 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
   double best_cost = 1e300;
   const int sms = h->sm_count;
   const bool nn = (opa == OP_N && opb == OP_N);
-  if (sums && M >= kRuleMinM && g_force_cfg < 0 && g_force_split <= 0)
+  if (sums && M >= rule_min_m() && g_force_cfg < 0 && g_force_split <= 0)
     return choose_sums_rule(M, N, K);
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
