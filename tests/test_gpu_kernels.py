@@ -428,7 +428,7 @@ def test_filter_with_sum_planes(eng, cfg, split):
     try:
         assert lib.chfsi_gemm_override(cfg, split) == 0
         # sum planes need n % 8 == 0 (3-D A boxes); a ragged n takes the plain 3M kernels
-        sizes = [(304, 37, 6), (1000, 120, 5), (136, 1, 3)]
+        sizes = [(304, 37, 6), (1000, 120, 5), (136, 1, 3), (8, 1, 4), (16, 3, 2), (24, 40, 3)]
         if cfg < _SUMS_FIRST:
             sizes.append((301, 37, 6))
         for (n, k, m) in sizes:
