@@ -1,5 +1,5 @@
 """First-contact GPU probe: GEMM op correctness vs torch (CPU), peaks, filter-step rates."""
-import json, sys, time
+import json, sys
 import numpy as np
 import torch
 sys.path.insert(0, ".")

@@ -22,7 +22,6 @@ import json
 import math
 import sys
 
-import numpy as np
 
 N_ORDER = 20000
 DEGREE = 25

@@ -5,7 +5,7 @@ from OpenBLAS, so 1e-13 instead of bit equality)."""
 import numpy as np
 import pytest
 
-from conftest import gapped_matrix, rand_hermitian, rand_spd, spectrum_matrix
+from conftest import rand_hermitian, rand_spd, spectrum_matrix
 
 pytestmark = pytest.mark.gpu
 
