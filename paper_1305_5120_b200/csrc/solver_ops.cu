@@ -126,7 +126,7 @@ struct FilterSums {
 };
 
 static int filter_sums(Handle* h, long long n, long long k, const double2* H, long long ldh,
-                       const double2* Y, long long ldy, FilterSums* fs) {
+                       const double2* Y, long long ldy, FilterSums* fs, bool h_plane = true) {
   *fs = FilterSums{};
   if (complex_mul() != 3 || n <= 0 || k <= 0 || n % 8 != 0) return OK;
   const long long ld = (n + 1) & ~1LL;
@@ -138,7 +138,8 @@ static int filter_sums(Handle* h, long long n, long long k, const double2* H, lo
   fs->Ys = (double*)scratch(h, SLOT_YSUM, (size_t)2 * ld * k * sizeof(double));
   if (!fs->Hs || !fs->Ys) return ERR_NOMEM;
   fs->Ws = fs->Ys + ld * k;
-  if (!declared) CHFSI_TRY(sum_plane_grouped(h, n, n, H, ldh, fs->Hs));
+  // (h_plane = false: the caller fills Hs itself -- the streamed filter, panel by panel)
+  if (!declared && h_plane) CHFSI_TRY(sum_plane_grouped(h, n, n, H, ldh, fs->Hs));
   return sum_plane(h, n, k, Y, ldy, fs->Ys, ld);
 }
 
@@ -272,6 +273,11 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     ev.push_back(e);
   }
   const std::vector<double> coef = filter_coefs(degree, a, b, lam_ref);
+  // 3M sum planes: Y's now, H's panel by panel as its rows land, the first step's
+  // output plane from the panel epilogues -- so the first step runs the sum-plane
+  // kernels too and no full-H plane pass follows the upload
+  FilterSums fs;
+  CHFSI_TRY(filter_sums(h, n, k, H, ldh, Y, ldy, &fs, /*h_plane=*/false));
   // the destination may still be read by earlier work queued on the compute stream
   CHFSI_CUDA(cudaEventRecord(ev[panels], h->stream));
   CHFSI_CUDA(cudaStreamWaitEvent(h->copy_stream, ev[panels], 0));
@@ -286,13 +292,18 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     // copy call returns only once staged, and the step of panel p then overlaps the
     // staging of panel p + 1
     CHFSI_CUDA(cudaStreamWaitEvent(h->stream, ev[p], 0));
-    CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0], coef[1],
-                                 nullptr, 0, 0.0, W + r0, ldw, nullptr));
+    if (fs.Hs != nullptr) {
+      // grouped plane rows [r0, r0 + m) start at group r0 / 8 (r0, m multiples of 8)
+      double* hs_panel = fs.Hs + r0 * n;
+      CHFSI_TRY(sum_plane_grouped(h, m, n, H + r0, ldh, hs_panel));
+      SumPlanes sp{hs_panel, 0, fs.Ys, fs.ldy, fs.Ws + r0, fs.ldy};
+      CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0],
+                                   coef[1], nullptr, 0, 0.0, W + r0, ldw, nullptr, &sp));
+    } else {
+      CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0],
+                                   coef[1], nullptr, 0, 0.0, W + r0, ldw, nullptr));
+    }
   }
-  // 3M sum planes once all of H is in: Hs and the plane of the first step's output W
-  FilterSums fs;
-  CHFSI_TRY(filter_sums(h, n, k, H, ldh, W, ldw, &fs));
-  std::swap(fs.Ys, fs.Ws);
   CHFSI_TRY(filter_steps(h, n, k, degree, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, W,
                          result_in_w, &fs));
   // everything is queued; return once the host buffer has been read so the caller
