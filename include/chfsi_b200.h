@@ -95,6 +95,17 @@ int chfsi_filter_streamed(chfsi_handle_t h, int64_t n, int64_t k, int degree, do
                           int64_t ldh, void* d_Y, int64_t ldy, void* d_W, int64_t ldw, int panels,
                           int* h_result_in_w);
 
+/* chfsi_filter_streamed that also returns the result to the host: the last degree step
+ * runs by row panels and each panel of p_m(H) Y is copied to h_out (column-major,
+ * ld_out >= n; page-locked for full speed) while the next panel computes. Returns once
+ * the result is in h_out (the whole of `chebyshev_filter(ndarray H, ndarray Y, spec)`,
+ * core.py:287-311, host to host; d_Y / d_W still hold the device result as flagged). */
+int chfsi_filter_streamed_to_host(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a,
+                                  double b, double lam_ref, const void* h_H, int64_t ldh_host,
+                                  void* d_H, int64_t ldh, void* d_Y, int64_t ldy, void* d_W,
+                                  int64_t ldw, int panels, void* h_out, int64_t ld_out,
+                                  int* h_result_in_w);
+
 /* One fused degree step C = alpha H Y1 + beta Y1 + gamma Y0 (Y0 may be NULL and may
  * alias C); the unit the filter roofline is measured on (core.py:280-281). */
 int chfsi_filter_step(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,

@@ -47,6 +47,9 @@ SIGNATURES = {
     "chfsi_filter_streamed": (_int, [_c_void_p, _i64, _i64, _int, _dbl, _dbl, _dbl, _c_void_p,
                                       _i64, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64,
                                       _int, _pint]),
+    "chfsi_filter_streamed_to_host": (_int, [_c_void_p, _i64, _i64, _int, _dbl, _dbl, _dbl,
+                                              _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i64,
+                                              _c_void_p, _i64, _int, _c_void_p, _i64, _pint]),
     "chfsi_filter_step": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _i64, _dbl,
                                   _dbl, _c_void_p, _i64, _dbl, _c_void_p, _i64]),
     "chfsi_lanczos_bound": (_int, [_c_void_p, _i64, _int, _c_void_p, _i64, _c_void_p, _pdbl,

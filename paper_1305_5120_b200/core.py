@@ -333,10 +333,14 @@ def _filter_streamed(host_h, Y, spec):
         raise ContractViolation(f"filter operand mismatch: H is {(n, n)}, Y has {dev.rows(yb)} rows")
     hdev = dev.empty(n, n, device)
     w = torch.empty_like(yb)
-    out = engine(device).filter_streamed(host_h, hdev, yb, w, spec.degree, spec.a, spec.b,
-                                         spec.lam_ref)
+    # the result comes back to the host panel by panel under the last degree step
+    out, host = engine(device).filter_streamed_to_host(host_h, hdev, yb, w, spec.degree,
+                                                       spec.a, spec.b, spec.lam_ref)
     _count_products(spec.degree * dev.cols(yb))
-    return VectorBlock(out)
+    vb = VectorBlock(out)
+    host.setflags(write=False)
+    object.__setattr__(vb, "_host", host)
+    return vb
 
 
 def _filter_sharded(H, Y, spec, group):

@@ -62,7 +62,7 @@ int filter(Handle* h, long long n, long long k, int degree, double a, double b, 
 int filter_streamed(Handle* h, long long n, long long k, int degree, double a, double b,
                     double lam_ref, const double2* H_host, long long ldh_host, double2* H,
                     long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
-                    int panels, int* result_in_w);
+                    int panels, int* result_in_w, double2* out_host, long long ld_out);
 int cholesky_inverse(Handle* h, long long k, double2* G, long long ldg, double shift,
                      double2* Li, long long ldli, double* diag_host, double* trace_host,
                      int* info_host);
@@ -292,7 +292,26 @@ int chfsi_filter_streamed(chfsi_handle_t h, int64_t n, int64_t k, int degree, do
   }
   return filter_streamed(h, n, k, degree, a, b, lam_ref, (const double2*)h_H, ldh_host,
                          (double2*)d_H, ldh, (double2*)d_Y, ldy, (double2*)d_W, ldw, panels,
-                         h_result_in_w);
+                         h_result_in_w, nullptr, 0);
+}
+
+int chfsi_filter_streamed_to_host(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a,
+                                  double b, double lam_ref, const void* h_H, int64_t ldh_host,
+                                  void* d_H, int64_t ldh, void* d_Y, int64_t ldy, void* d_W,
+                                  int64_t ldw, int panels, void* h_out, int64_t ld_out,
+                                  int* h_result_in_w) {
+  H_CHECK(h);
+  if (!(a < b)) {
+    set_error("filter interval requires a < b");
+    return ERR_ARG;
+  }
+  if (!h_H || !d_H || !h_out) {
+    set_error("filter_streamed_to_host: null H or output");
+    return ERR_ARG;
+  }
+  return filter_streamed(h, n, k, degree, a, b, lam_ref, (const double2*)h_H, ldh_host,
+                         (double2*)d_H, ldh, (double2*)d_Y, ldy, (double2*)d_W, ldw, panels,
+                         h_result_in_w, (double2*)h_out, ld_out);
 }
 
 int chfsi_filter_step(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H, int64_t ldh,

@@ -241,10 +241,22 @@ static int filter_issue(Handle* h, long long n, long long k, int degree, const d
 // panel is in. With pinned host memory the upload (PCIe) hides behind the first step
 // except for one panel. Every panel step accumulates each output over K in the same
 // order as the full-height step, so the result is identical when no panel uses split-K.
+// Rows [r0, r0 + m) of a device block (column-major, ld) to the same rows of a host
+// block, on the copy stream once the compute stream has produced them (event `ev`).
+static int panel_to_host(Handle* h, cudaEvent_t ev, const double2* src, long long lds,
+                         long long m, long long k, double2* dst, long long ldd) {
+  CHFSI_CUDA(cudaEventRecord(ev, h->stream));
+  CHFSI_CUDA(cudaStreamWaitEvent(h->copy_stream, ev, 0));
+  CHFSI_CUDA(cudaMemcpy2DAsync(dst, (size_t)ldd * sizeof(double2), src,
+                               (size_t)lds * sizeof(double2), (size_t)m * sizeof(double2),
+                               (size_t)k, cudaMemcpyDeviceToHost, h->copy_stream));
+  return OK;
+}
+
 int filter_streamed(Handle* h, long long n, long long k, int degree, double a, double b,
                     double lam_ref, const double2* H_host, long long ldh_host, double2* H,
                     long long ldh, double2* Y, long long ldy, double2* W, long long ldw,
-                    int panels, int* result_in_w) {
+                    int panels, int* result_in_w, double2* out_host, long long ld_out) {
   if (degree < 1) {
     set_error("filter degree must be >= 1");
     return ERR_ARG;
@@ -253,7 +265,7 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     *result_in_w = 0;
     return OK;
   }
-  if (ldh_host < n || ldh < n) {
+  if (ldh_host < n || ldh < n || (out_host != nullptr && ld_out < n)) {
     set_error("filter_streamed: leading dimensions must be >= n");
     return ERR_ARG;
   }
@@ -267,7 +279,9 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
     CHFSI_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   if (!h->copy_events) h->copy_events = new std::vector<cudaEvent_t>();
   auto& ev = *h->copy_events;
-  while ((int)ev.size() < panels + 1) {
+  // events: [0, panels) H panels landed, [panels] stream fence, [panels + 1 + p] output
+  // panel p computed (D2H of the last step)
+  while ((int)ev.size() < 2 * panels + 1) {
     cudaEvent_t e;
     CHFSI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev.push_back(e);
@@ -303,12 +317,40 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
       CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, Y, ldy, Y + r0, ldy, coef[0],
                                    coef[1], nullptr, 0, 0.0, W + r0, ldw, nullptr));
     }
+    if (out_host != nullptr && degree == 1)
+      CHFSI_TRY(panel_to_host(h, ev[panels + 1 + p], W + r0, ldw, m, k, out_host + r0, ld_out));
   }
-  CHFSI_TRY(filter_steps(h, n, k, degree, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, W,
-                         result_in_w, &fs));
+  if (out_host == nullptr || degree == 1) {
+    CHFSI_TRY(filter_steps(h, n, k, degree, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw, W,
+                           result_in_w, &fs));
+  } else {
+    // steps 2 .. degree - 1, then the last step by row panels, each panel read back to
+    // the host on the copy stream while the next panel computes
+    int in_w = 1;
+    CHFSI_TRY(filter_steps(h, n, k, degree - 1, 1, coef.data(), nullptr, H, ldh, Y, ldy, W, ldw,
+                           W, &in_w, &fs));
+    double2* cur = in_w ? W : Y;
+    double2* prev = in_w ? Y : W;
+    const long long ldc = in_w ? ldw : ldy, ldp = in_w ? ldy : ldw;
+    double* s_cur = fs.Hs ? (in_w ? fs.Ws : fs.Ys) : nullptr;
+    const int j = degree - 1;
+    for (int p = 0; p < panels; ++p) {
+      const long long r0 = p * rows;
+      const long long m = std::min(rows, n - r0);
+      SumPlanes sp{fs.Hs ? fs.Hs + r0 * n : nullptr, 0, s_cur, fs.ldy, nullptr, 0};
+      CHFSI_TRY(zgemm_filter_panel(h, m, k, n, H + r0, ldh, cur, ldc, cur + r0, ldc,
+                                   coef[3 * j], coef[3 * j + 1], prev + r0, ldp,
+                                   coef[3 * j + 2], prev + r0, ldp, nullptr,
+                                   fs.Hs ? &sp : nullptr));
+      CHFSI_TRY(panel_to_host(h, ev[panels + 1 + p], prev + r0, ldp, m, k, out_host + r0, ld_out));
+    }
+    *result_in_w = (prev == W) ? 1 : 0;
+  }
   // everything is queued; return once the host buffer has been read so the caller
-  // may free or reuse it (the GPU keeps filtering meanwhile)
+  // may free or reuse it (the GPU keeps filtering meanwhile) -- or, with out_host, once
+  // the result has landed there
   CHFSI_CUDA(cudaEventSynchronize(ev[panels - 1]));
+  if (out_host != nullptr) CHFSI_CUDA(cudaStreamSynchronize(h->copy_stream));
   return OK;
 }
 

@@ -175,6 +175,24 @@ class Engine:
                      ptr(W), ld(W), int(panels), ctypes.byref(flag))
         return W if flag.value else Y
 
+    def filter_streamed_to_host(self, host_H, H, Y, W, degree, a, b, lam_ref, panels=0):
+        """filter_streamed whose result also lands in a page-locked host array, panel by
+        panel during the last degree step (chfsi_filter_streamed_to_host). Returns
+        (device tensor holding the result, F-order (n, k) host array)."""
+        if not (isinstance(host_H, np.ndarray) and host_H.dtype == np.complex128
+                and host_H.flags.f_contiguous and host_H.ndim == 2):
+            raise ValueError("filter_streamed: host_H must be an F-contiguous complex128 matrix")
+        n, k = rows(Y), cols(Y)
+        if host_H.shape != (n, n) or rows(H) != n or cols(H) != n:
+            raise ValueError("filter_streamed: H must be n x n with n = rows(Y)")
+        out = torch.empty((k, n), dtype=torch.complex128, pin_memory=True)
+        flag = ctypes.c_int(0)
+        _native.call("chfsi_filter_streamed_to_host", self.h, n, k, int(degree), float(a),
+                     float(b), float(lam_ref), host_H.ctypes.data, n, ptr(H), ld(H), ptr(Y),
+                     ld(Y), ptr(W), ld(W), int(panels), ctypes.c_void_p(out.data_ptr()), n,
+                     ctypes.byref(flag))
+        return (W if flag.value else Y), out.numpy().T
+
     @staticmethod
     def complex_mul():
         """Complex-product scheme of the TMA GEMMs: 3 (3M) or 4 real products."""

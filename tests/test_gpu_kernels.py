@@ -114,6 +114,46 @@ def test_filter_streamed_matches_oracle(eng, n, k, m, panels):
     assert np.array_equal(D.to_host(dH), h)
 
 
+@pytest.mark.parametrize("n,k,m,panels", [(512, 37, 7, 3), (1000, 120, 1, 4), (1000, 64, 2, 0),
+                                          (136, 1, 3, 1)])
+def test_filter_streamed_to_host(eng, n, k, m, panels):
+    """Host-to-host filter (H streamed in, the last degree step by row panels with each
+    panel read back under the next): the host result equals the device result bit for
+    bit and the oracle recurrence to rounding; degree 1 reads back the first step's
+    panels."""
+    import oracle.chfsi_oracle as O
+    from paper_1305_5120_b200 import device as D
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    h, lam, _ = baseline_matrix(n, n)
+    h = np.asfortranarray(h)
+    rng = np.random.default_rng(n + 5 * k + m)
+    y = crand(rng, n, k)
+    a, b, lam_ref = float(lam[min(k, n - 1)]), float(lam[-1]) * 1.05, float(lam[0])
+    ref = O.cheb_filter(h, y, m, a, b, lam_ref)
+    dH = D.empty(n, n, eng.device)
+    dev_out, host = eng.filter_streamed_to_host(h, dH, D.to_device(y, eng.device),
+                                                D.zeros(n, k, eng.device), m, a, b, lam_ref,
+                                                panels=panels)
+    assert np.array_equal(host, D.to_host(dev_out))
+    assert np.linalg.norm(host - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_public_filter_host_operator_to_host(eng):
+    """chebyshev_filter(ndarray H >= 4096, ndarray Y) -- the bench's e2e path: entries are
+    already on the host when the call returns and match the oracle."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    n, k, m = 4096, 24, 3
+    h, lam, _ = baseline_matrix(n, n)
+    y = crand(np.random.default_rng(8), n, k)
+    spec = G.FilterSpec(degree=m, a=float(lam[k]), b=float(lam[-1]) * 1.05, lam_ref=float(lam[0]))
+    out = G.chebyshev_filter(np.asfortranarray(h), y, spec)
+    assert out._host is not None
+    ref = O.cheb_filter(h, y, m, spec.a, spec.b, spec.lam_ref)
+    assert np.linalg.norm(out.entries - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
 def test_filter_streamed_bit_identical_without_split(eng):
     """With split-K off, every panel step sums each output over K in the order of the
     full-height step: the streamed filter equals the resident one bit for bit."""
