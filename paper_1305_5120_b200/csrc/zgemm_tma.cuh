@@ -99,7 +99,7 @@ constexpr int kDefer = CHFSI_TMA_DEFER;
 // warp tile, release the stage, and (rotating producer lane) refill the stage that
 // was released one iteration earlier.
 template <int BM, int BN, int WM, int WN, int STAGES, int MUL, bool SUMS, bool RAGGED, class Issue>
-__device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2* sA,
+__device__ __forceinline__ void tma_mainloop(const double2* sA,
                                              const double2* sB, const double* sAs,
                                              const double* sBs, uint64_t* full, uint64_t* empty,
                                              Issue& issue, int KT, int wm, int wn, int lane,
@@ -111,7 +111,6 @@ __device__ __forceinline__ void tma_mainloop(const GemmParams& p, const double2*
   constexpr int NWARP = (BM / WM) * (BN / WN);
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
-  (void)p;
   // unrolled by the ring depth: the stage index, its smem addresses and barrier slots
   // become compile-time constants in each copy (ncu: DMMA pipe 95.5 -> 97.4 % for the
   // sum-plane filter kernel, 47.1 -> 48.2 TF/s at k = 2200)
@@ -315,9 +314,8 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       if (s < KT) issue(s);
   }
 
-  const int fr = lane >> 2, fc = lane & 3;
-  const int pr = perm8(fr);
-  (void)fr;
+  const int fc = lane & 3;
+  const int pr = perm8(lane >> 2);
   // 8-column MMA blocks of this warp that hold at least one real column: blocks
   // entirely past N (the padded tail of a narrow filter block) issue no DMMAs.
   // Warp-uniform, so DMMA's warp-collective semantics are kept.
@@ -334,10 +332,10 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int t = 0; t < 2; ++t) c0[i][j][t] = c1[i][j][t] = c2[i][j][t] = 0.0;
 
   if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, false>(p, sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, false>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                     lane, warp, fc, pr, jvalid, c0, c1, c2);
   } else {  // ragged column edge: skip 8-column blocks past N
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, true>(p, sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, true>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                    lane, warp, fc, pr, jvalid, c0, c1, c2);
   }
 
