@@ -45,7 +45,7 @@ for k in widths:
     W = torch.empty_like(Y)
     row = {}
     splits = (1, 2, 3, 4, 6, 8, 12, 17) if k <= 300 else (1, 2, 3) if k <= 1200 else (1,)
-    for c in ((14, 15, 16) if os.environ.get("SUMS_ONLY") else (11, 12, 14, 15, 16)):
+    for c in (tuple(int(x) for x in os.environ["CFGS"].split(",")) if os.environ.get("CFGS") else (14, 15, 16) if os.environ.get("SUMS_ONLY") else (11, 12, 14, 15, 16)):
         for s in splits:
             lib.chfsi_gemm_override(c, s)
             row[f"c{c}s{s}"] = round(run(k, Y, W), 2)
