@@ -133,48 +133,86 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU legs
-def cpu_filter_rate(n, degree, seconds, seed=0):
-    """Oracle CPU filter (numpy zgemm via OpenBLAS, all cores) on a bounded
-    column sample; returns (TFLOP/s, sample description, cores)."""
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return {d.get("internal_api", "?"): d.get("num_threads") for d in threadpool_info()
+                if d.get("user_api") == "blas"}
+    except Exception:  # pragma: no cover - informational only
+        return {}
+
+
+def host_operands(n, k, seed=0):
+    """The GPU arm's operands on the host: H from the c0 spectrum recipe at order n,
+    generated exactly as the GPU arm generates it (workloads.spectrum_matrix_torch on
+    cuda:0 -- torch QR/matmul, data generation only, none of this repo's kernels), the
+    start block Y (n x k, torch generator seed 1234) and the spectrum. Without a GPU
+    (CPU tests) H follows the host recipe (workloads.baseline_matrix)."""
+    import torch
+    from paper_1305_5120_b200 import workloads as Wl
+    if torch.cuda.is_available():
+        dev = torch.device("cuda", torch.cuda.current_device())
+        H, lam = Wl.spectrum_matrix_torch(seed, n, dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234)
+        Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
+        h = H.cpu().numpy().T  # (k, n) row j = column j -> F-order n x n
+        del H
+        y = Y.cpu().numpy().T
+        del Y
+        torch.cuda.empty_cache()
+        return h, y, lam, "c0 spectrum recipe, generated on the GPU exactly as the b200 arm"
+    h, lam, _ = Wl.baseline_matrix(seed, n)
+    rng = np.random.default_rng(1234)
+    y = np.asfortranarray(rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)))
+    return h, y, lam, "c0 spectrum recipe (host numpy; no GPU visible)"
+
+
+def filter_params(lam, k):
+    nev = int(round(k * 2000 / 2200))
+    return float(lam[0]), float(lam[min(nev, len(lam) - 1)]), 1.01 * float(lam[-1])
+
+
+def cpu_filter_rate(h, y, lam, seconds):
+    """Oracle CPU filter (the reference's recurrence, numpy zgemm via OpenBLAS on all host
+    threads) on the bench's own H and full k-column block, one degree step per call,
+    repeated until ``seconds`` have elapsed; returns (TFLOP/s, sample, cores)."""
     import oracle.chfsi_oracle as O
-    rng = np.random.default_rng(seed)
-    # the operator's values do not change the zgemm cost: a seeded complex
-    # Gaussian Hermitian stands in for the c4 matrix on the host
-    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
-    h = np.asfortranarray((g + g.conj().T) * (0.5 / np.sqrt(n)))
-    del g
-    ks = 32
-    y = rng.standard_normal((n, ks)) + 1j * rng.standard_normal((n, ks))
-    O.cheb_filter(h, y, 1, 0.5, 3.0, -3.0)  # warm-up (thread pool, page faults)
-    done_flops, t_used, calls = 0.0, 0.0, 0
+    n, k = y.shape
+    lam_ref, a_edge, b_up = filter_params(lam, k)
+    O.cheb_filter(h, y[:, :32], 1, a_edge, b_up, lam_ref)  # warm-up (thread pool, pages)
+    done, t_used, calls = 0.0, 0.0, 0
     while t_used < seconds and calls < 50:
         t0 = time.perf_counter()
-        O.cheb_filter(h, y, 2, 0.5, 3.0, -3.0)
+        O.cheb_filter(h, y, 1, a_edge, b_up, lam_ref)
         t_used += time.perf_counter() - t0
-        done_flops += 8.0 * n * n * ks * 2
+        done += 8.0 * n * n * k
         calls += 1
     cores = os.cpu_count()
-    sample = (f"oracle cheb_filter, n={n}, {ks} of {2200} columns, degree 2 per call, {calls} calls "
-              f"({t_used:.1f} s), numpy/OpenBLAS zgemm on {cores} host threads")
-    return done_flops / t_used / 1e12, sample, cores
+    sample = (f"oracle cheb_filter (core.py:263-284 restated) on the bench's H (n={n}) and full "
+              f"{k}-column block, one degree step per call, {calls} calls ({t_used:.1f} s), "
+              f"numpy/OpenBLAS on {cores} host threads {blas_threads()}")
+    return done / t_used / 1e12, sample, cores
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (oracle port) on the host cores."""
+    """--impl reference: the reference algorithm's filter (oracle restatement of
+    core.py:263-284: numpy zgemm on OpenBLAS, all host threads) on the b200 arm's own
+    workload -- the same H (c0 recipe, n), the same full k-column block -- one degree step
+    per step (the b200 arm's step is a degree-m call: same_config differs only in the
+    degree; the unit is per-flop). Rank 0 alone runs it; other ranks exit 0."""
     if rank != 0:
         return
     import oracle.chfsi_oracle as O
-    n = args.n
-    rng = np.random.default_rng(0)
-    g = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
-    h = np.asfortranarray((g + g.conj().T) * (0.5 / np.sqrt(n)))
-    del g
-    ks = 32
-    y = rng.standard_normal((n, ks)) + 1j * rng.standard_normal((n, ks))
-    step_flops = 8.0 * n * n * ks * 1
+    n, k = args.n, args.k
+    t0 = time.perf_counter()
+    h, y, lam, recipe = host_operands(n, k)
+    t_gen = time.perf_counter() - t0
+    lam_ref, a_edge, b_up = filter_params(lam, k)
+    step_flops = 8.0 * n * n * k
 
     def step():
-        O.cheb_filter(h, y, 1, 0.5, 3.0, -3.0)
+        O.cheb_filter(h, y, 1, a_edge, b_up, lam_ref)
 
     for _ in range(args.warmup):
         step()
@@ -184,17 +222,19 @@ def run_reference(args, rank, world):
     dt = time.perf_counter() - t0
     val = step_flops * args.steps / dt / 1e12
     cores = os.cpu_count()
+    sample = (f"one full-width filter degree step per step (zgemm n={n} x k={k} + recurrence), "
+              f"oracle restatement of core.py:263-284, numpy/OpenBLAS on {cores} threads "
+              f"{blas_threads()}")
     line = {
         "impl": "reference", "metric": metric_name(args), "value": val, "unit": UNIT,
         "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
-        "data": "synthetic (seeded complex Gaussian Hermitian; c4 shape)",
-        "config": dict(workload_cfg(args, 1), sample_columns=ks),
+        "data": f"synthetic (seeded; H = Q diag(lambda) Q^H, {recipe})",
+        "config": dict(workload_cfg(args, 1), degree_per_step=1, same_config=True,
+                       setup_s=t_gen),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"one filter degree step (zgemm n={n} x {ks} of 2200 columns + "
-                                   f"recurrence) per step, oracle restatement of core.py:263-284, "
-                                   f"numpy/OpenBLAS on {cores} threads"},
+                         "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -367,6 +407,9 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
         other = 4 if args.complex_mul == 3 else 3
         leg(f"filter_complex_mul_{other}",
             lambda: filter_other_mul(eng, H, Y0, Y, W, m, a_edge, b_up, lam_ref, other))
+        # host copies for the CPU baseline leg (the same H and full block)
+        h_host = H.cpu().numpy().T
+        y_host = Yfull.cpu().numpy().T
         del Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         nev_s = int(round(args.k * 2000 / 2200))
@@ -379,9 +422,10 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
         leg("generalized_c4_setup", generalized_c4_setup)
 
         def cpu_leg():
-            rate, sample, cores = cpu_filter_rate(n, m, args.cpu_seconds)
+            rate, sample, cores = cpu_filter_rate(h_host, y_host, lam, args.cpu_seconds)
             return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
         leg("cpu_baseline", cpu_leg)
+        del h_host, y_host
     print(json.dumps(line), flush=True)
 
 
@@ -697,15 +741,44 @@ def tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref, degree=5):
     return out
 
 
+def oracle_c0_solve(limit_s=240.0):
+    """The reference algorithm (oracle restatement of core.py:385-546, numpy/OpenBLAS on
+    all host cores + the C Jacobi) solving BASELINE config 0 in full on this box's CPU,
+    in the same run (generator seed 0, solver seed 1). Runs in a child process under a
+    time limit so a slow host cannot cost the headline line."""
+    code = ("import json, os, sys, time; sys.path.insert(0, %r); "
+            "import oracle.chfsi_oracle as O; "
+            "from paper_1305_5120_b200.workloads import baseline_matrix; "
+            "h, lam_true, _ = baseline_matrix(0, 1000); t0 = time.perf_counter(); "
+            "lam, v, rep = O.solve(h, None, 100, 20, 15, 1e-10, 20000, seed=1); "
+            "dt = time.perf_counter() - t0; "
+            "print(json.dumps({'s': dt, 'iterations': len(rep['iterations']), "
+            "'total_matmuls': int(rep['total_matmuls']), 'lam': [float(x) for x in lam]}))"
+            % ROOT)
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             timeout=limit_s, cwd=ROOT)
+    except subprocess.TimeoutExpired:
+        return {"error": f"oracle c0 solve exceeded {limit_s:.0f} s"}
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    if out.returncode != 0 or not lines:
+        return {"error": (out.stderr or "no output")[-300:]}
+    d = json.loads(lines[-1])
+    d["cores"] = os.cpu_count()
+    d["blas_threads"] = blas_threads()
+    d["kind"] = "port"
+    return d
+
+
 def solve_c0():
     """s per ChFSI solve at BASELINE config 0 (n=1000, nev=100, nex=20, m=15, random start;
-    generator seed 0, solver seed 1). The reference CPU needed 2524 iterations / 60.6 s
-    here (tests/golden/c0.npz). Reported for the reference interval placement and for the
-    opt-in block_top placement (SURVEY.md section 7 ii)."""
+    generator seed 0, solver seed 1), for the reference interval placement and for the
+    opt-in block_top placement (SURVEY.md section 7 ii), with the reference algorithm's
+    own full CPU solve timed on this box's host cores in the same run (oracle)."""
     import paper_1305_5120_b200 as G
     from paper_1305_5120_b200.workloads import baseline_matrix
     h, lam_true, _ = baseline_matrix(0, 1000)
-    out = {"reference_cpu_s": 60.6, "reference_cpu_iterations": 2524}
+    out = {}
     for interval in ("reference", "block_top"):
         cfg = G.SolverConfig(nev=100, buffer=20, degree=15, max_outer_iters=20000,
                              interval=interval)
@@ -717,12 +790,41 @@ def solve_c0():
             "total_matmuls": rep.total_matmuls,
             "max_rel_eig_err_vs_exact": float(np.max(np.abs(lam - lam_true[:100]) / np.abs(lam_true[:100]))),
             "t_filter": rep.t_filter, "t_qr": rep.t_qr, "t_rr": rep.t_rr}
+        if interval == "reference":
+            lam_gpu = lam
+    cpu = oracle_c0_solve()
+    if "lam" in cpu:
+        ref = np.asarray(cpu.pop("lam"))
+        cpu["max_rel_eig_diff_gpu_vs_cpu"] = float(np.max(np.abs(lam_gpu - ref) / np.abs(ref)))
+        out["reference_cpu_s"] = cpu["s"]
+        out["reference_cpu_iterations"] = cpu["iterations"]
+        out["speedup_vs_cpu"] = cpu["s"] / out["reference"]["s_per_solve"]
+    out["reference_cpu"] = cpu
     return out
+
+
+def oracle_c1_sample(probs, limit_iters=80):
+    """CPU side of the c1 leg: the oracle solving c1 problem 1 (reference RNG order: the
+    solver Generator [seed, 11, 1]) for a bounded number of outer iterations on this
+    box's cores; returns (seconds, matmul-columns done) for a per-column extrapolation."""
+    import oracle.chfsi_oracle as O
+    tally = O.Tally()
+    t0 = time.perf_counter()
+    try:
+        O.solve(probs[0][0], None, 200, 40, 20, 1e-10, limit_iters,
+                seed=np.random.default_rng([0, 11, 1]), tally=tally)
+    except O.OracleError:
+        pass  # NotConverged after the bounded sample: expected
+    dt = time.perf_counter() - t0
+    return dt, int(tally.cols)
 
 
 def sequence_c1():
     """BASELINE config 1: 5 correlated n=2000 problems (delta = 1e-3 ||H_1||), nev=200, nex=40,
-    m=20, eigenvector reuse through solve_sequence; s per sequence (reference CPU: ~999 s)."""
+    m=20, eigenvector reuse through solve_sequence; s per sequence. CPU: the oracle's time per
+    matmul-column on a bounded sample of problem 1 (same box, same run) times the
+    sequence's total work (which equals the reference's: tests/golden/c1_full.npz),
+    labelled as extrapolated."""
     import paper_1305_5120_b200 as G
     from paper_1305_5120_b200.workloads import baseline_sequence
     probs = baseline_sequence(0, 2000, 5)
@@ -732,16 +834,77 @@ def sequence_c1():
     t0 = time.perf_counter()
     rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
     dt = time.perf_counter() - t0
-    return {"s_per_sequence": dt, "reference_cpu_s": 999.0,
-            "iterations": [r.outer_iterations for r in rep.reports],
-            "work": rep.work, "filter_s": sum(r.t_filter for r in rep.reports)}
+    out = {"s_per_sequence": dt,
+           "iterations": [r.outer_iterations for r in rep.reports],
+           "work": rep.work, "filter_s": sum(r.t_filter for r in rep.reports)}
+    gold = os.path.join(ROOT, "tests", "golden", "c1_full.npz")
+    if os.path.exists(gold):
+        g = np.load(gold)
+        out["max_rel_eig_diff_vs_reference"] = max(
+            float(np.max(np.abs(lam - g[f"lam{i}"]) / np.abs(g[f"lam{i}"])))
+            for i, lam in enumerate(rep.eigenvalues))
+        out["reference_iterations"] = [int(len(g[f"it_filtered{i}"])) for i in range(5)]
+    try:
+        t_s, cols = oracle_c1_sample(probs)
+        total = float(sum(rep.work))
+        out["reference_cpu"] = {
+            "s_extrapolated": t_s / max(cols, 1) * total, "kind": "port",
+            "cores": os.cpu_count(), "blas_threads": blas_threads(),
+            "sample": f"oracle solve of problem 1, first 80 outer iterations: {cols} "
+                      f"matmul-columns in {t_s:.1f} s, scaled to the sequence's {int(total)}"}
+        out["reference_cpu_s"] = out["reference_cpu"]["s_extrapolated"]
+    except Exception as exc:  # pragma: no cover - reported
+        out["reference_cpu"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+    return out
+
+
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launcher_argv(argv, n):
+    """The torch.distributed.run command that starts ``n`` ranks of this script with the
+    same arguments (one process per GPU, rendezvous on 127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+            os.path.abspath(__file__)] + list(argv)
+
+
+def check_visible_gpus(args):
+    """--gpus N over NCCL needs N distinct GPUs; fail loudly instead of measuring fewer."""
+    if args.impl != "b200" or args.dist_backend != "nccl":
+        return None
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < args.gpus:
+        return f"--gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}"
+    return None
 
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        sys.exit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # started without a launcher: start the N ranks ourselves (the driver's
+        # `bench.py --gpus N` and a torchrun launch measure the same thing)
+        err = check_visible_gpus(args)
+        if err:
+            sys.exit(f"bench.py: {err}")
+        proc = subprocess.run(launcher_argv(sys.argv[1:], args.gpus))
+        sys.exit(proc.returncode)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1 and local_rank == 0:
+        err = check_visible_gpus(args)
+        if err:
+            sys.exit(f"bench.py: {err}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

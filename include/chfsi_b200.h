@@ -228,6 +228,23 @@ int chfsi_apply_operator(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H
 int chfsi_peak_dmma(int device, int iters, double* h_tflops);
 int chfsi_peak_dfma(int device, int iters, double* h_tflops);
 
+/* In-process multi-GPU (SURVEY.md section 8b `chfsi_ctx_create(ndev, devices)`): one
+ * NCCL clique over `ndev` distinct GPUs of this process (ncclCommInitAll), one rank per
+ * device, each driven by its own host thread. The reference takes its parallelism
+ * in-process (linalg.py:49-64 `set_workers`, the column tiles of linalg.py:238-243);
+ * here the filter columns are sharded over the clique (H replicated) and the shards are
+ * all-gathered for QR and Rayleigh-Ritz (distributed.py). NCCL is dlopen'ed at first
+ * use; chfsi_comm_available() reports whether it loads (and its version code). */
+typedef struct chfsi_comm_s* chfsi_comm_t;
+int chfsi_comm_available(int* h_version);
+int chfsi_comm_init_all(int ndev, const int* h_devices, chfsi_comm_t* h_out);
+int chfsi_comm_destroy(chfsi_comm_t c);
+int chfsi_comm_abort(chfsi_comm_t c);
+/* d_recv (world * bytes) <- every rank's d_send (bytes) in rank order, on `stream` */
+int chfsi_comm_allgather(chfsi_comm_t c, const void* d_send, void* d_recv, size_t bytes,
+                         void* stream);
+int chfsi_comm_broadcast(chfsi_comm_t c, void* d_buf, size_t bytes, int root, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

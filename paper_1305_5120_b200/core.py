@@ -253,14 +253,19 @@ def _lanczos(hm, k, rng):
     return bound
 
 
-def chebyshev_filter(H, Y, spec, *, group=None):
+def chebyshev_filter(H, Y, spec, *, group=None, devices=None):
     """p_m(H) Y with the scaled Chebyshev recurrence (core.py:287-311).
 
     ``group`` (keyword-only, B200 extension): a torch.distributed process group with
     one process per GPU. Every rank passes the same H and Y; a host H is uploaded as
     one column slab per rank and all-gathered over NVLink, each rank filters its
     contiguous column range of Y, and the filtered shards are all-gathered, so every
-    rank returns the full p_m(H) Y."""
+    rank returns the full p_m(H) Y. ``devices`` (keyword-only): the same over several
+    GPUs of THIS process (an int N or CUDA ordinals; one thread per GPU, NCCL clique);
+    the result lives on the first device."""
+    if devices is not None:
+        return _in_process(devices, group, lambda comm, _rng: chebyshev_filter(
+            _localize(H), _localize(Y), spec, group=comm), None)
     if not isinstance(spec, FilterSpec):
         if all(hasattr(spec, f) for f in ("degree", "a", "b", "lam_ref")):
             spec = FilterSpec(spec.degree, spec.a, spec.b, spec.lam_ref)
@@ -651,15 +656,72 @@ class DeviceSolver:
         return vals, VectorBlock(out, orthonormal=True), report
 
 
-def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None, callback=None):
+def _localize(x, memo=None):
+    """Per-rank view of an argument inside an in-process rank thread (``devices=``):
+    device-resident matrices and blocks are copied to the thread's own GPU (over
+    NVLink) and wrapped anew, so ranks never share (or flip) a wrapper's device cache;
+    host arrays pass through (each rank uploads its own copy). ``memo`` maps id(x) to
+    the local copy, so an object used by several problems (a sequence's fixed B, whose
+    Cholesky factor is cached) is localised once per rank."""
+    if memo is not None and id(x) in memo:
+        return memo[id(x)]
+    out = x
+    d = default_device()
+    if isinstance(x, HermitianDenseMatrix):
+        if x._dev is not None:
+            blk = x._dev if x._dev.device == d else x._dev.to(d)
+            out = HermitianDenseMatrix.from_device(blk, trusted=True)
+        else:
+            out = HermitianDenseMatrix(x)  # host-backed: uploads on this rank's device
+    elif isinstance(x, VectorBlock) and x._dev is not None:
+        blk = x._dev if x._dev.device == d else x._dev.to(d)
+        out = VectorBlock(blk)
+        object.__setattr__(out, "orthonormal", x.orthonormal)
+    elif isinstance(x, torch.Tensor) and x.is_cuda and x.device != d:
+        out = x.to(d)
+    if memo is not None:
+        memo[id(x)] = out
+    return out
+
+
+def _in_process(devices, group, fn, seed):
+    """Run ``fn(comm, seed_copy)`` on one thread per GPU of ``devices`` (comm.py) and
+    return rank 0's result. Every rank gets its own copy of the caller's Generator (the
+    start block and rank-collapse columns are replicated draws); afterwards the
+    caller's Generator is left where rank 0's ended, as after a one-GPU solve."""
+    from .comm import clone_rng, normalize_devices, run_on_devices
+    if group is not None:
+        raise ContractViolation("give either group= (one process per GPU) or devices= "
+                                "(several GPUs in this process), not both")
+    devs = normalize_devices(devices)
+    rngs = [clone_rng(seed) for _ in devs]
+    if len(devs) == 1:
+        with torch.cuda.device(devs[0]):
+            out = fn(None, rngs[0])
+    else:
+        out = run_on_devices(devs, lambda comm: fn(comm, rngs[comm.rank]))[0]
+    if isinstance(seed, np.random.Generator):
+        seed.bit_generator.state = rngs[0].bit_generator.state
+    return out
+
+
+def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None, devices=None,
+                callback=None):
     """Run ChFSI on a standard Hermitian problem (core.py:385-546).
 
     Same signature, return types, report fields, RNG order and exceptions
     as the reference; arithmetic on the GPU. ``group`` (keyword-only, B200
     extension): a torch.distributed process group with one process per GPU;
     the filter columns are then sharded across its ranks (H replicated).
+    ``devices`` (keyword-only): the same sharded solve over several GPUs of this
+    process -- an int N (GPUs 0..N-1) or CUDA ordinals; one host thread per GPU and
+    an NCCL clique (comm.py); results on the first device.
     ``callback`` (keyword-only, B200 extension): called with each IterationStat.
     """
+    if devices is not None:
+        return _in_process(devices, group, lambda comm, rng: chfsi_solve(
+            _localize(H), _localize(Y0), config, prior, rng, group=comm,
+            callback=callback if comm is None or comm.rank == 0 else None), seed)
     config = _as_config(config)
     if isinstance(H, HermitianDenseMatrix):
         n = H.n
@@ -689,10 +751,16 @@ def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None, callback=None)
     return DeviceSolver(hm, config, group=group).run(y0, prior, rng, callback)
 
 
-def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, callback=None):
+def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, devices=None,
+                      callback=None):
     """A c = lambda B c for the nev lowest pairs (core.py:549-569):
     B = L L^H (cuSOLVER zpotrf), H = L^-1 A L^-H (triangular inverse + DMMA
-    GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors."""
+    GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors.
+    ``group`` / ``devices``: as for chfsi_solve."""
+    if devices is not None:
+        return _in_process(devices, group, lambda comm, rng: solve_generalized(
+            _localize(A), _localize(B), _localize(Y0), config, prior, rng, group=comm,
+            callback=callback if comm is None or comm.rank == 0 else None), seed)
     config = _as_config(config)
     ab = A.device_block() if isinstance(A, HermitianDenseMatrix) else None
     bb = B.device_block() if isinstance(B, HermitianDenseMatrix) else None

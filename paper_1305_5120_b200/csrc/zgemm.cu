@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cmath>
 #include <string>
+#include <mutex>
 #include <unordered_map>
 
 #include "internal.h"
@@ -154,6 +155,10 @@ struct Entry {
 };
 Entry g_table[NCFG][2][2][3];
 bool g_table_init = false;
+// cudaFuncSetAttribute is per device: the devices whose attributes are set (bit i =
+// ordinal i; one process may drive several GPUs, one engine per device)
+unsigned long long g_table_devices = 0;
+std::mutex g_table_mu;
 
 template <class C, int OPA, int OPB, int EPI>
 void put(int ci) {
@@ -184,8 +189,43 @@ void put_tma(int ci) {
   }
 }
 
+void fill_table();
+
 int ensure_table() {
+  int dev = 0;
+  CHFSI_CUDA(cudaGetDevice(&dev));
+  const unsigned long long bit = (dev < 64) ? (1ULL << dev) : 0ULL;
+  std::lock_guard<std::mutex> lock(g_table_mu);
+  if (g_table_init && (g_table_devices & bit)) return OK;
+  if (!g_table_init) fill_table();
+  for (int c = 0; c < NCFG; ++c)
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b)
+        for (int e = 0; e < 3; ++e) {
+          Entry& en = g_table[c][a][b][e];
+          if (!en.fn) continue;
+          CHFSI_CUDA(cudaFuncSetAttribute((const void*)en.fn,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem));
+          if (g_table_init) continue;  // occupancy: the same on every B200
+          int occ = 0;
+          CHFSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)en.fn,
+                                                                   en.threads, en.smem));
+          en.occ = std::max(occ, 1);
+          en.ready = true;
+        }
+  g_table_devices |= bit;
   if (g_table_init) return OK;
+  g_table_init = true;
+  if (getenv("CHFSI_PLAN_DEBUG")) {
+    for (int c = 0; c < NCFG; ++c)
+      fprintf(stderr, "chfsi cfg %d: occ NN store %d filter %d partial %d, CN store %d partial %d\n", c,
+              g_table[c][0][0][0].occ, g_table[c][0][0][1].occ, g_table[c][0][0][2].occ,
+              g_table[c][1][0][0].occ, g_table[c][1][0][2].occ);
+  }
+  return OK;
+}
+
+void fill_table() {
   put_all<C0>(0);
   put_all<C1>(1);
   put_all<C2>(2);
@@ -203,28 +243,6 @@ int ensure_table() {
   put_tma<T14>(14);
   put_tma<T15>(15);
   put_tma<T16>(16);
-  for (int c = 0; c < NCFG; ++c)
-    for (int a = 0; a < 2; ++a)
-      for (int b = 0; b < 2; ++b)
-        for (int e = 0; e < 3; ++e) {
-          Entry& en = g_table[c][a][b][e];
-          if (!en.fn) continue;
-          CHFSI_CUDA(cudaFuncSetAttribute((const void*)en.fn,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, en.smem));
-          int occ = 0;
-          CHFSI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)en.fn,
-                                                                   en.threads, en.smem));
-          en.occ = std::max(occ, 1);
-          en.ready = true;
-        }
-  g_table_init = true;
-  if (getenv("CHFSI_PLAN_DEBUG")) {
-    for (int c = 0; c < NCFG; ++c)
-      fprintf(stderr, "chfsi cfg %d: occ NN store %d filter %d partial %d, CN store %d partial %d\n", c,
-              g_table[c][0][0][0].occ, g_table[c][0][0][1].occ, g_table[c][0][0][2].occ,
-              g_table[c][1][0][0].occ, g_table[c][1][0][2].occ);
-  }
-  return OK;
 }
 
 struct Plan {
@@ -339,7 +357,8 @@ Plan choose_sums_rule(long long M, long long N, long long K) {
 }
 
 Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
-            bool sums) {
+            bool sums, bool tma = true) {
+  tma = tma && g_tma_enabled;
   Plan best;
   double best_cost = 1e300;
   const int sms = h->sm_count;
@@ -348,11 +367,11 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
     return choose_sums_rule(M, N, K);
   for (int c = 0; c < NCFG; ++c) {
     if (g_force_cfg >= 0 && c != g_force_cfg) continue;
-    if (c >= FIRST_TMA && !g_tma_enabled) continue;
+    if (c >= FIRST_TMA && !tma) continue;
     if (g_force_cfg < 0 && c >= FIRST_TMA && (c >= FIRST_3M) != (g_mul == 3)) continue;
     // 3M on: every op N x N product runs a 3M kernel (the cp.async kernels use four
     // products), so the rounding of a product does not depend on the planner's pick
-    if (g_force_cfg < 0 && nn && g_mul == 3 && g_tma_enabled && K > 0 && c < FIRST_3M) continue;
+    if (g_force_cfg < 0 && nn && g_mul == 3 && tma && K > 0 && c < FIRST_3M) continue;
     // operand-sum planes: only (and always) the sum-reading kernels; never without planes
     if (c >= FIRST_SUMS && !sums && g_force_cfg < 0) continue;
     if (g_force_cfg < 0 && sums && c < FIRST_SUMS) continue;
@@ -387,11 +406,11 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
 // per-call host cost of a small GEMM is a hash lookup (the solve's tail issues
 // thousands of identical small products).
 struct PlanKey {
-  int opa, opb, epi, fcfg, fsplit, mul, sums;
+  int opa, opb, epi, fcfg, fsplit, mul, sums, tma, sms;
   long long M, N, K;
   bool operator==(const PlanKey& o) const {
     return opa == o.opa && opb == o.opb && epi == o.epi && fcfg == o.fcfg && fsplit == o.fsplit &&
-           mul == o.mul && sums == o.sums &&
+           mul == o.mul && sums == o.sums && tma == o.tma && sms == o.sms &&
            M == o.M && N == o.N && K == o.K;
   }
 };
@@ -401,18 +420,25 @@ struct PlanKeyHash {
     h ^= (size_t)k.N * 0xC2B2AE3D27D4EB4FULL + (h << 6) + (h >> 2);
     h ^= (size_t)k.K * 0x165667B19E3779F9ULL + (h << 6) + (h >> 2);
     h ^= (size_t)(k.opa | (k.opb << 1) | (k.epi << 2) | ((k.fcfg + 1) << 4) | (k.fsplit << 9) |
-                  (k.mul << 16) | (k.sums << 20));
+                  (k.mul << 16) | (k.sums << 20) | (k.tma << 21) | ((size_t)k.sms << 22));
     return h;
   }
 };
 
 Plan cached_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, long long K,
-                 bool sums) {
+                 bool sums, bool tma = true) {
+  // shared by every handle (one per device, possibly on several host threads)
   static std::unordered_map<PlanKey, Plan, PlanKeyHash> cache;
-  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, g_mul, sums ? 1 : 0, M, N, K};
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  const Plan pl = choose(h, opa, opb, epi, M, N, K, sums);
+  static std::mutex mu;
+  const PlanKey key{opa, opb, epi, g_force_cfg, g_force_split, g_mul, sums ? 1 : 0, tma ? 1 : 0,
+                    h->sm_count, M, N, K};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const Plan pl = choose(h, opa, opb, epi, M, N, K, sums, tma);
+  std::lock_guard<std::mutex> lock(mu);
   if (cache.size() > 65536) cache.clear();
   cache.emplace(key, pl);
   return pl;
@@ -560,9 +586,12 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
+  // the TMA kernels load whole 8-column K tiles and cannot mask a triangular K bound
+  // that is not a multiple of 8 (the cp.async kernels mask every element)
+  const bool tma = g_tma_enabled && !(p.tri != 0 && (p.tri_off & 7) != 0);
   const bool sums = p.As != nullptr && p.Bs != nullptr && g_mul == 3 && opa == OP_N &&
-                    opb == OP_N && g_tma_enabled && M % 8 == 0;
-  const Plan pl = cached_plan(h, opa, opb, epi, M, N, K, sums);
+                    opb == OP_N && tma && M % 8 == 0;
+  const Plan pl = cached_plan(h, opa, opb, epi, M, N, K, sums, tma);
   const int c = pl.cfg;
   p.a3d = (M % 8 == 0) ? 1 : 0;  // one 3-D A box per stage (TMA kernels)
   if (c >= FIRST_SUMS && !sums) {

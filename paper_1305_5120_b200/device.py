@@ -11,6 +11,7 @@ in libchfsi_b200.so, reached through :class:`Engine`.
 """
 
 import ctypes
+import threading
 import warnings
 
 import numpy as np
@@ -30,8 +31,25 @@ def cols(t):
     return t.shape[0] if t.dim() == 2 else 1
 
 
+def _check_layout(t):
+    """A (k, n) block must be column-major: unit stride along rows (the kernels read
+    column j at data_ptr + j * ld) and ld >= n; a transposed or strided view would be
+    read with the wrong layout."""
+    if t.dim() == 2 and t.shape[1] > 1 and t.stride(1) != 1:
+        raise ValueError(f"block has row stride {t.stride(1)}; the kernels need unit stride "
+                         f"along rows (a (cols, rows) tensor with contiguous columns)")
+    if t.dim() == 2 and t.shape[0] > 1 and t.stride(0) < t.shape[1]:
+        raise ValueError(f"block leading dimension {t.stride(0)} < rows {t.shape[1]}")
+    if t.dim() == 1 and t.shape[0] > 1 and t.stride(0) != 1:
+        raise ValueError("vector must be contiguous")
+
+
 def ld(t):
-    return t.stride(0) if t.dim() == 2 else t.shape[0]
+    _check_layout(t)
+    if t.dim() != 2:
+        return t.shape[0]
+    # a single column's stride is arbitrary in torch: report the row count then
+    return t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[1])
 
 
 def ptr(t):
@@ -42,6 +60,7 @@ def ptr(t):
         return ctypes.c_void_p(0)
     if t.is_conj() or t.is_neg():
         raise ValueError("tensor has a lazy conj/neg bit; call resolve_conj()/resolve_neg() first")
+    _check_layout(t)
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -85,10 +104,25 @@ def to_host(t):
     return np.asfortranarray(t.to("cpu").numpy().T)
 
 
+_tls = threading.local()
+
+
+def set_engine_tag(tag):
+    """Engines are per (device, tag); the in-process multi-GPU runner (comm.py) gives
+    each rank thread its own tag, so ranks never share a handle's scratch arenas (two
+    ranks may even share one GPU in the tests)."""
+    _tls.tag = int(tag)
+
+
+def engine_tag():
+    return getattr(_tls, "tag", 0)
+
+
 class Engine:
     """Native handle bound to one CUDA device and torch's current stream there."""
 
     _engines = {}
+    _lock = threading.Lock()
 
     def __init__(self, device):
         if not torch.cuda.is_available():
@@ -111,12 +145,16 @@ class Engine:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
         idx = device.index if device.index is not None else torch.cuda.current_device()
-        eng = cls._engines.get(idx)
+        key = (idx, engine_tag())
+        eng = cls._engines.get(key)
         cur = torch.cuda.current_stream(idx)
         if eng is None:
-            eng = cls(torch.device("cuda", idx))
-            cls._engines[idx] = eng
-        elif eng.stream.cuda_stream != cur.cuda_stream:
+            with cls._lock:
+                eng = cls._engines.get(key)
+                if eng is None:
+                    eng = cls(torch.device("cuda", idx))
+                    cls._engines[key] = eng
+        if eng.stream.cuda_stream != cur.cuda_stream:
             eng.stream = cur
             _native.call("chfsi_set_stream", eng.h, ctypes.c_void_p(cur.cuda_stream))
         return eng

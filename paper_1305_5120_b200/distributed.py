@@ -1,4 +1,4 @@
-"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL on B200).
+"""Multi-GPU plumbing: H replicated, filter columns sharded, all-gathers only.
 
 The filter is column-separable (core.py:276-283 touches each column on its
 own), so the active block is split into contiguous column ranges exactly like
@@ -7,12 +7,19 @@ H is replicated on every rank and there is no communication inside the
 filter. After the filter the shards are all-gathered (NCCL over NVLink) for
 CholQR and Rayleigh-Ritz.
 
-All collectives here are plain torch.distributed calls, so the same code runs
-on CPU tensors under the gloo backend in the tests (world_size 2).
+``group`` anywhere below is either a torch.distributed process group (one
+process per GPU, e.g. torchrun; gloo on CPU in the tests) or an in-process
+:class:`comm.ThreadComm` (one thread per GPU, NCCL clique; ``devices=`` on the
+public entry points). Both expose the same four collectives (comm.py).
 """
 
+import hashlib
+
+import numpy as np
 import torch
-import torch.distributed as dist
+
+from .comm import as_comm, world_of
+from .errors import ChfsiError
 
 
 class ColumnShards:
@@ -52,7 +59,8 @@ class ColumnShards:
         if self.world == 1:
             gathered[: local.shape[0]].copy_(local)
             return gathered
-        rank = dist.get_rank(group)
+        comm = as_comm(group)
+        rank = comm.rank
         w = self.widths[rank]
         if local.shape[0] != w:
             raise ValueError(f"rank {rank} shard has {local.shape[0]} columns, expected {w}")
@@ -61,12 +69,7 @@ class ColumnShards:
         else:
             send = torch.zeros((self.padded, local.shape[1]), dtype=local.dtype, device=local.device)
             send[:w].copy_(local)
-        if _needs_host_staging(send, group):
-            recv = torch.empty(gathered.shape, dtype=gathered.dtype)
-            dist.all_gather_into_tensor(recv, send.cpu(), group=group)
-            gathered.copy_(recv)
-        else:
-            dist.all_gather_into_tensor(gathered, send, group=group)
+        comm.all_gather_into_tensor(gathered, send)
         return gathered
 
     def compact(self, gathered, out):
@@ -88,34 +91,55 @@ class ColumnShards:
         return self.compact(g, out)
 
 
-def _needs_host_staging(t, group):
-    return t.is_cuda and dist.get_backend(group) == "gloo"
-
-
 def world_info(group=None):
-    """(rank, world) of ``group``; (0, 1) when torch.distributed is not initialised."""
-    if not dist.is_available() or not dist.is_initialized():
-        return 0, 1
-    return dist.get_rank(group), dist.get_world_size(group)
+    """(rank, world) of ``group``; (0, 1) when there is none."""
+    return world_of(group)
 
 
-def all_gather_values(vals, shards, group=None):
-    """Gather per-rank 1-D float64 vectors (e.g. residual norms of own columns)."""
+def all_gather_values(vals, shards, group=None, extra=None):
+    """Gather per-rank 1-D float64 vectors (e.g. residual norms of own columns).
+    ``extra``: a few float64 values per rank gathered in the same collective; returns
+    (values, extras (world, len(extra))) when given."""
     if shards.world == 1:
-        return vals
-    rank = dist.get_rank(group)
+        return vals if extra is None else (vals, np.asarray([extra], dtype=np.float64))
+    comm = as_comm(group)
+    rank = comm.rank
     w = shards.widths[rank]
-    stage = _needs_host_staging(vals, group)
-    dev = torch.device("cpu") if stage else vals.device
-    send = torch.zeros(shards.padded, dtype=torch.float64, device=dev)
+    ne = 0 if extra is None else len(extra)
+    width = shards.padded + ne
+    dev = torch.device("cpu") if comm.host_staging(vals) else vals.device
+    send = torch.zeros(width, dtype=torch.float64, device=dev)
     send[:w].copy_(vals[:w])
-    recv = torch.empty(shards.padded * shards.world, dtype=torch.float64, device=dev)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    if ne:
+        send[shards.padded:].copy_(torch.as_tensor(np.asarray(extra, dtype=np.float64)))
+    recv = torch.empty(width * shards.world, dtype=torch.float64, device=dev)
+    comm.all_gather_into_tensor(recv, send)
     out = torch.empty(shards.k, dtype=torch.float64, device=vals.device)
     for r in range(shards.world):
         lo, hi = shards.range(r)
-        out[lo:hi].copy_(recv[r * shards.padded: r * shards.padded + hi - lo])
-    return out
+        out[lo:hi].copy_(recv[r * width: r * width + hi - lo])
+    if extra is None:
+        return out
+    ex = recv.view(shards.world, width)[:, shards.padded:].cpu().numpy()
+    return out, ex
+
+
+def fingerprint(*arrays):
+    """Exact 48-bit fingerprint (as a float64) of host arrays' bytes: equal on two ranks
+    iff (up to hash collisions) the arrays are bit-identical."""
+    h = hashlib.blake2b(digest_size=6)
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return float(int.from_bytes(h.digest(), "little"))
+
+
+def check_agreement(extras, what):
+    """Every rank's row of ``extras`` must be bit-identical (replicated decisions)."""
+    ex = np.asarray(extras)
+    if ex.shape[0] > 1 and not np.all(ex == ex[0]):
+        raise ChfsiError(f"cross-rank divergence in {what}: the replicated values differ "
+                         f"between ranks ({ex.tolist()}); the sharded solve cannot continue "
+                         f"consistently")
 
 
 class ShardedPhases:
@@ -142,9 +166,40 @@ class ShardedPhases:
     """
 
     def __init__(self, group=None):
-        self.group = group
-        self.rank, self.world = world_info(group)
+        self.comm = as_comm(group)
+        self.group = self.comm
+        self.rank, self.world = world_info(self.comm)
         self._bufs = {}
+        self._weights = None
+        # test hook: (rank, callable(G)) applied to that rank's gathered RR Gram
+        self._perturb_gram = None
+
+    def agree(self, what, values, like):
+        """Cross-rank consistency guard for the replicated k x k decisions (Cholesky
+        branch and rank test, zheevd's Ritz values/vectors, hence the locking count):
+        they rely on bit-identical gathered inputs and deterministic kernels on every
+        GPU. All-gather a few float64 values and raise ChfsiError on every rank when
+        any rank differs, instead of letting the ranks take different branches (which
+        would hang or corrupt the next collective)."""
+        vals = np.asarray(values, dtype=np.float64).ravel()
+        dev = torch.device("cpu") if self.comm.host_staging(like) else like.device
+        send = torch.as_tensor(vals).to(dev)
+        recv = torch.empty(vals.size * self.world, dtype=torch.float64, device=dev)
+        self.comm.all_gather_into_tensor(recv, send)
+        check_agreement(recv.view(self.world, vals.size).cpu().numpy(), what)
+
+    def _w_fingerprint(self, W):
+        """Deterministic device reduction of W (k x k eigenvectors) to k doubles: a bit
+        flip anywhere in W changes them (up to rounding coincidences)."""
+        k = W.shape[0]
+        if self._weights is None or self._weights.shape[0] < 2 * k or \
+                self._weights.device != W.device:
+            g = torch.Generator(device="cpu")
+            g.manual_seed(97)
+            self._weights = torch.rand(2 * max(k, 1), generator=g,
+                                       dtype=torch.float64).to(W.device)
+        wv = torch.view_as_real(W).reshape(k, 2 * k)
+        return (wv * self._weights[:2 * k]).sum(dim=1).cpu().numpy()
 
     def _scratch(self, name, k, n, like):
         buf = self._bufs.get(name)
@@ -198,6 +253,8 @@ class ShardedPhases:
 
         gram(F)
         d1, tr, info1 = eng.cholesky_inverse(G, Li)
+        # the branch below must be the same on every rank
+        self.agree("CholQR2 first Cholesky", [info1, tr, fingerprint(d1)], F)
         fro = float(np.sqrt(max(tr, 0.0)))
         if info1 != 0:
             # first Cholesky broke down: shifted CholQR3 (Fukaya et al.),
@@ -221,11 +278,14 @@ class ShardedPhases:
             d2, _, info2 = eng.cholesky_inverse(G, Li)
             apply(T, Q)
             infos, diags = (info1, info2), (d1, d2)
+        r = np.abs(np.prod(np.stack(diags), axis=0))
+        bad = np.nonzero(r < rank_tol * fro)[0]
+        # one decision on every rank (or a clean error on all of them)
+        self.agree("CholQR2 rank test", list(infos) + [int(bad[0]) if bad.size else -1,
+                                                      fingerprint(r)], F)
         for info in infos:
             if info != 0:
                 raise RankDeficient(int(info) - 1)
-        r = np.abs(np.prod(np.stack(diags), axis=0))
-        bad = np.nonzero(r < rank_tol * fro)[0]
         if bad.size:
             raise RankDeficient(int(bad[0]))
         return Q
@@ -246,6 +306,8 @@ class ShardedPhases:
         if w_:
             eng.zgemm("C", "N", k, w_, n, 1.0, Q, HQ[lo:hi], 0.0, W[lo:hi])
         self._gather(sh, W[lo:hi], W)
+        if self._perturb_gram is not None and self._perturb_gram[0] == self.rank:
+            self._perturb_gram[1](W)
         eng.hermitize(W)
         lam = eng.heevd(W)  # W <- eigenvectors, ascending
         if w_:
@@ -254,8 +316,12 @@ class ShardedPhases:
             mine = eng.residual_norms(HZ[lo:hi], Z[lo:hi], lam[lo:hi])
         else:
             mine = np.empty(0)
-        res = all_gather_values(torch.from_numpy(np.ascontiguousarray(mine)).to(Q.device), sh,
-                                self.group)
+        # the Ritz values and vectors are replicated decisions: their fingerprints ride
+        # along with the residual gather (no extra collective)
+        res, ex = all_gather_values(torch.from_numpy(np.ascontiguousarray(mine)).to(Q.device),
+                                    sh, self.group,
+                                    extra=[fingerprint(lam), fingerprint(self._w_fingerprint(W))])
+        check_agreement(ex, "Rayleigh-Ritz (zheevd Ritz values / vectors)")
         return lam, res.cpu().numpy(), W
 
     def ritz_columns(self, eng, Q, W, kk, locked_out, z):

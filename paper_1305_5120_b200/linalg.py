@@ -58,6 +58,8 @@ def product_count():
 
 def _count_products(cols):
     global _product_columns
+    if dev.engine_tag() != 0:
+        return  # in-process ranks (comm.py): the work is counted once, by rank 0
     with _lock:
         _product_columns += int(cols)
 
