@@ -355,6 +355,10 @@ def run_b200(args, rank, world, local_rank):
                                                                  nev_s, k - nev_s, m))
             if rank == 0:
                 line["solve_c4"] = solve
+            for key, fn in extra_solve_legs(H, lam, rank, world, dev, nev_s, k - nev_s, m):
+                out = guarded_leg(line, rank, fn, key=key)
+                if rank == 0:
+                    line[key] = out
         if rank == 0:
             print(json.dumps(line), flush=True)
         return
@@ -415,6 +419,9 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
         nev_s = int(round(args.k * 2000 / 2200))
         line["solve_c4"] = guarded_leg(line, 0, lambda: solve_c4_leg(
             H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree))
+        for key, fn in extra_solve_legs(H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree):
+            line[key] = guarded_leg(line, 0, fn, key=key)
+            torch.cuda.empty_cache()
         del H
         torch.cuda.empty_cache()
         leg("solve_c0", solve_c0)
@@ -453,7 +460,7 @@ KERNELS = {
 SOLVE_LEG_LIMIT_S = 900.0
 
 
-def guarded_leg(line, rank, fn, limit_s=SOLVE_LEG_LIMIT_S):
+def guarded_leg(line, rank, fn, limit_s=SOLVE_LEG_LIMIT_S, key="solve_c4"):
     """Run a leg that has collectives inside on every rank. An exception is reported in
     the line; a leg still running after limit_s (e.g. a rank stuck in a collective
     after another rank failed) makes rank 0 print the headline line with the error and
@@ -462,7 +469,7 @@ def guarded_leg(line, rank, fn, limit_s=SOLVE_LEG_LIMIT_S):
 
     def fire():
         if rank == 0 and line is not None:
-            line["solve_c4"] = {"error": f"leg exceeded {limit_s:.0f} s; abandoned"}
+            line[key] = {"error": f"leg exceeded {limit_s:.0f} s; abandoned"}
             print(json.dumps(line), flush=True)
         os._exit(0)
 
@@ -514,6 +521,187 @@ def solve_c4_leg(H, lam, rank, world, dev, nev=2000, nex=200, degree=25):
             "filter_share": tf / dt,
             "residuals_below_tol": bool(rep.converged),
             "max_rel_eig_err_vs_exact": float(np.max(np.abs(vals - lam[:nev]) / np.abs(lam[:nev])))}
+
+
+def extra_solve_legs(H, lam, rank, world, dev, nev, nex, degree):
+    """The legs that run on every rank after solve_c4 (column-sharded for N > 1)."""
+    return [("solve_c4_reference_window",
+             lambda: reference_window_leg(H, lam, rank, world, dev, nev, nex, degree)),
+            ("sequence_c4", lambda: sequence_c4_leg(H, lam, rank, world, dev, nev, nex, degree))]
+
+
+# c4 standard problem 1 with the reference's own interval semantics (profiles/r01/solves/
+# c4_standard_problem1_reference_interval_3m.json, one B200): 5024 outer iterations, of
+# which this many ran at full width (k_a > 1000) and the rest in the narrow tail
+REF_TRACE = os.path.join(ROOT, "profiles", "r01", "solves",
+                         "c4_standard_problem1_reference_interval_3m.json")
+
+
+def reference_window_leg(H, lam, rank, world, dev, nev=2000, nex=200, degree=25, head=3,
+                         tail=40, tail_cols=201):
+    """A bounded window of the c4 solve under the reference's own interval semantics
+    (a = Ritz value nev+1, core.py:507-509), timed at every N (max over ranks):
+    * head: the solve's first ``head`` outer iterations at full width (chfsi_solve with
+      max_outer_iters = head; its NotConverged report carries the iteration times);
+    * tail: ``tail`` iterations of the long narrow tail that dominates this solve
+      (k_a ~ 201 columns against 2000 locked vectors), timed from a synthetic state
+      (DeviceSolver.probe_iterations: random orthonormal locked block, random active
+      block; the per-iteration work does not depend on the values);
+    and the whole-solve estimate t_head x (full-width iterations of the one-GPU trace)
+    + t_tail x (its narrow iterations)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.core import DeviceSolver
+    n = H.shape[0]
+    grp = dist.group.WORLD if world > 1 else None
+    if world > 1:
+        dist.broadcast(H, src=0)
+    hm = G.HermitianDenseMatrix.from_device(H, trusted=True)
+    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=degree, max_outer_iters=head,
+                         interval="reference")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    try:
+        G.chfsi_solve(hm, None, cfg, seed=1, group=grp)
+        its = None
+    except G.NotConverged as exc:
+        its = exc.report.iterations
+    torch.cuda.synchronize()
+    t_head_total = time.perf_counter() - t0
+    head_iter = [i.t_filter + i.t_qr + i.t_rr for i in (its or [])]
+    # tail state (replicated: generated from one seed and broadcast)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77)
+    locked = torch.linalg.qr(torch.randn((n, nev), dtype=torch.complex128, device=dev,
+                                         generator=g))[0]
+    locked = locked.T.contiguous()  # (nev, n): column-major n x nev block
+    active = torch.randn((tail_cols, n), dtype=torch.complex128, device=dev, generator=g)
+    if world > 1:
+        dist.broadcast(locked, src=0)
+        dist.broadcast(active, src=0)
+    solver = DeviceSolver(hm, cfg, group=grp)
+    b_up = 1.01 * float(lam[-1])
+    solver.probe_iterations(locked, active, 2, float(lam[nev]), b_up, float(lam[0]))  # warm
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    per = solver.probe_iterations(locked, active, tail, float(lam[nev]), b_up, float(lam[0]))
+    torch.cuda.synchronize()
+    t_tail_total = time.perf_counter() - t0
+    vals = [t_head_total / max(1, len(head_iter)), t_tail_total / tail,
+            sum(p[0] for p in per) / tail, sum(p[1] for p in per) / tail,
+            sum(p[2] for p in per) / tail]
+    tt = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_head, t_tail, tf, tq, trr = [float(x) for x in tt]
+    out = {"n": n, "nev": nev, "nex": nex, "degree": degree, "interval": "reference",
+           "n_gpus": world, "head_iterations": len(head_iter),
+           "s_per_head_iteration": t_head, "tail_iterations": tail, "tail_cols": tail_cols,
+           "s_per_tail_iteration": t_tail,
+           "tail_phase_s": {"filter": tf, "qr": tq, "rr": trr}}
+    try:
+        with open(REF_TRACE) as f:
+            trace = json.load(f)["problems"][0]["iterations"]
+        wide = sum(1 for it in trace if it[0] > 1000)
+        narrow = len(trace) - wide
+        if (n, nev, nex, degree) == (20000, 2000, 200, 25):
+            out["est_s_per_solve"] = wide * t_head + narrow * t_tail
+            out["est_basis"] = (f"one-GPU reference-interval trace: {wide} full-width + "
+                                f"{narrow} narrow iterations (measured 1-GPU solve 2007 s)")
+    except Exception:  # pragma: no cover - informational
+        pass
+    return out
+
+
+def sequence_c4_leg(H, lam, rank, world, dev, nev=2000, nex=200, degree=25, problems=2):
+    """The north star's target sequence, bounded to ``problems`` problems: BASELINE c4
+    generalized (S = I + 0.1 B^H B / ||B^H B||, A_1 = the bench's H, A_{l+1} = A_l +
+    delta E_l with delta = 1e-3 ||A_1||), eigenvector reuse, through the drop-in
+    solve_sequence(seq, config, "reuse", group=) -- column-sharded over the ranks for
+    N > 1 -- with the opt-in block_top interval; s per problem (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200 import device as D
+    n = H.shape[0]
+    eng = D.Engine.get(dev)
+    grp = dist.group.WORLD if world > 1 else None
+
+    def norm2(blk, seed):
+        v = np.random.default_rng(seed).standard_normal(n) + 0j
+        v /= np.linalg.norm(v)
+        return eng.lanczos_bound(blk, D.to_device(v, dev), 10)[0]
+
+    t0 = time.perf_counter()
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    b = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+    s = torch.empty_like(b)
+    eng.zgemm("C", "N", n, n, n, 1.0, b, b, 0.0, s)
+    del b
+    eng.hermitize(s)
+    s.mul_(0.1 / norm2(s, 4))
+    s.diagonal().add_(1.0)
+    mats = [H.clone()]
+    delta = 1e-3 * max(abs(float(lam[0])), abs(float(lam[-1])))
+    for ell in range(2, problems + 1):
+        g.manual_seed(100 + ell)
+        e = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+        e = ((e + e.conj().T) / 2).conj().resolve_conj().contiguous()
+        e.mul_(delta / norm2(e, 200 + ell))
+        mats.append(mats[-1] + e)
+        del e
+    if world > 1:  # the replicated decisions need bit-identical operators
+        dist.broadcast(s, src=0)
+        for a in mats:
+            dist.broadcast(a, src=0)
+    seq = G.ProblemSequence(
+        spec=G.SequenceSpec(n=n, N=problems, nev=nev, seed=0, kind="generalized"),
+        problems=[(G.HermitianDenseMatrix.from_device(a, trusted=True),
+                   G.HermitianDenseMatrix.from_device(s, trusted=True)) for a in mats])
+    # one S object for the whole sequence: its Cholesky factor is computed once
+    smat = seq.problems[0][1]
+    seq.problems = [(a, smat) for a, _ in seq.problems]
+    t_gen = time.perf_counter() - t0
+    cfg = G.SolverConfig(nev=nev, buffer=nex, degree=degree, max_outer_iters=2000,
+                         interval="block_top")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False, group=grp)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    tt = torch.tensor([dt] + [r.t_total for r in rep.reports], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    # verification of the last problem: generalized residuals and B-orthonormality
+    vb = rep.vectors[-1].device_block()
+    lamc = rep.eigenvalues[-1]
+    k = vb.shape[0]
+    av, sv = torch.empty_like(vb), torch.empty_like(vb)
+    eng.zgemm("N", "N", n, k, n, 1.0, mats[-1], vb, 0.0, av)
+    eng.zgemm("N", "N", n, k, n, 1.0, s, vb, 0.0, sv)
+    lt = torch.as_tensor(lamc, device=dev).to(vb.dtype)
+    res = float(torch.linalg.vector_norm(av - sv * lt[:, None], dim=1).max())
+    gram = torch.empty((k, k), dtype=vb.dtype, device=dev)
+    eng.zgemm("C", "N", k, k, n, 1.0, vb, sv, 0.0, gram)
+    orth = float(torch.linalg.matrix_norm(gram - torch.eye(k, dtype=vb.dtype, device=dev)))
+    return {"n": n, "nev": nev, "nex": nex, "degree": degree, "problems": problems,
+            "generalized": True, "interval": "block_top", "n_gpus": world,
+            "s_total": float(tt[0]), "s_per_problem": [float(x) for x in tt[1:]],
+            "outer_iterations": [r.outer_iterations for r in rep.reports],
+            "filter_tflops": [r.filter_tflops for r in rep.reports],
+            "t_lanczos": [r.t_lanczos for r in rep.reports],
+            "max_generalized_residual": res, "b_orthonormality": orth, "setup_s": t_gen,
+            "path": "solve_sequence(seq, cfg, 'reuse', group=WORLD)"}
 
 
 def plan_kernel_name(eng, n, k):

@@ -204,6 +204,49 @@ class ThreadComm(Comm):
         self._wait()
 
 
+_default_devices = None
+_tls = threading.local()
+
+
+def set_devices(devices):
+    """Default GPU set of the drop-in entry points when a call passes neither ``group=``
+    nor ``devices=`` (None or 1: one GPU). The GPU counterpart of the reference's
+    in-process worker knob (linalg.py:49-64 ``set_workers`` / ``CHFSI_WORKERS``); the
+    environment variable ``CHFSI_DEVICES`` (an int or a comma list) sets it too, so an
+    unmodified caller of ``chfsi_solve(H, None, config)`` runs on every listed GPU."""
+    global _default_devices
+    _default_devices = None if devices is None else normalize_devices(devices)
+
+
+def get_devices():
+    if _default_devices is not None:
+        return list(_default_devices)
+    env = __import__("os").environ.get("CHFSI_DEVICES", "").strip()
+    if not env:
+        return None
+    return normalize_devices(int(env) if env.isdigit() else [int(x) for x in env.split(",")])
+
+
+def default_devices():
+    """The default multi-GPU set for a drop-in call, or None (one GPU). Never inside a
+    rank thread of an in-process group (those calls carry their own ``group``)."""
+    if getattr(_tls, "inside", False):
+        return None
+    d = get_devices()
+    return d if d is not None and len(d) > 1 else None
+
+
+class inside_group:
+    """Context: calls made here do not pick up the default devices again."""
+
+    def __enter__(self):
+        self.prev = getattr(_tls, "inside", False)
+        _tls.inside = True
+
+    def __exit__(self, *exc):
+        _tls.inside = self.prev
+
+
 def normalize_devices(devices):
     """``devices``: an int N (GPUs 0..N-1) or a sequence of CUDA ordinals."""
     if isinstance(devices, int):
@@ -242,6 +285,7 @@ def run_on_devices(devices, fn, backend=None):
 
     def body(rank):
         d = devices[rank]
+        _tls.inside = True
         try:
             torch.cuda.set_device(d)
             dev.set_engine_tag(rank)

@@ -263,6 +263,8 @@ def chebyshev_filter(H, Y, spec, *, group=None, devices=None):
     rank returns the full p_m(H) Y. ``devices`` (keyword-only): the same over several
     GPUs of THIS process (an int N or CUDA ordinals; one thread per GPU, NCCL clique);
     the result lives on the first device."""
+    if devices is None and group is None:
+        devices = _default_devices()
     if devices is not None:
         return _in_process(devices, group, lambda comm, _rng: chebyshev_filter(
             _localize(H), _localize(Y), spec, group=comm), None)
@@ -499,6 +501,65 @@ class DeviceSolver:
     def _sync(self):
         self.eng.synchronize()
 
+    def _phases(self, act, ws, nl, a_edge, b_up, lam_ref, rng, ev):
+        """One outer iteration's arithmetic (core.py:459-477): filter the active block,
+        orthonormalise against the locked block, Rayleigh-Ritz + residual norms.
+        Phase times come from CUDA events on the solver stream: the iteration needs only
+        two host syncs (rank test after CholQR2; Ritz values + residuals)."""
+        ncols = dev.cols(act)
+        locked = ws.locked[:nl] if nl else None
+        ev[0].record(self.eng.stream)
+        f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref, locked)
+        ev[1].record(self.eng.stream)
+        _count_products(self.cfg.degree * ncols)
+        q = self._orthonormalize(f, locked, ws.hq[:ncols], ws.fa[:ncols], rng,
+                                 projected=self.sharded is not None)
+        ev[2].record(self.eng.stream)
+        wvec = None
+        if self.sharded is not None:
+            # f (in ws.fb) is dead after the QR: its buffer takes the own Ritz vectors
+            w, res, wvec = self.sharded.rayleigh_ritz(self.eng, self.hb, q, ws.hq[:ncols],
+                                                      ws.fb[:ncols], ws.hz[:ncols])
+        else:
+            w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
+                                            ws.hz[:ncols], residuals=True)
+        ev[3].record(self.eng.stream)
+        _count_products(ncols)
+        ev[3].synchronize()
+        tf = ev[0].elapsed_time(ev[1]) * 1e-3
+        tq = ev[1].elapsed_time(ev[2]) * 1e-3
+        trr = ev[2].elapsed_time(ev[3]) * 1e-3  # includes the fused residual norms
+        return q, w, res, wvec, tf, tq, trr
+
+    def probe_iterations(self, locked, active, iters, a_edge, b_up, lam_ref, seed=0):
+        """Time ``iters`` outer iterations from a given state -- ``locked`` (n x L,
+        orthonormal) and ``active`` (n x k) column-major device blocks -- without locking
+        (every iteration filters the current Ritz block again). The per-iteration cost
+        of a solve's long narrow tail (reference interval semantics, core.py:507-509: at
+        c4 ~5000 iterations at k_a ~ 201 with 2000 locked) without running the ~2000 s
+        solve; with a group the phases are sharded exactly as in a solve. Returns a list
+        of (t_filter, t_qr, t_rr, t_wall) per iteration."""
+        n = self.n
+        nl, k = dev.cols(locked), dev.cols(active)
+        ws = _Workspace(n, k, max(nl, 1), self.device)
+        ws.locked[:nl].copy_(locked)
+        ws.z[:k].copy_(active)
+        rng = _rng(seed)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        out = []
+        self.eng.declare_operator(self.hb)
+        try:
+            for _ in range(iters):
+                t0 = time.perf_counter()
+                q, w, res, wvec, tf, tq, trr = self._phases(ws.z[:k], ws, nl, a_edge, b_up,
+                                                            lam_ref, rng, ev)
+                if self.sharded is not None:
+                    self.sharded.ritz_columns(self.eng, q, wvec, 0, None, ws.z[:k])
+                out.append((tf, tq, trr, time.perf_counter() - t0))
+        finally:
+            self.eng.declare_operator(None)
+        return out
+
     # -- driver -------------------------------------------------------
     def run(self, Y0, prior, rng, callback=None):
         # H is not written during the solve: its 3M sum plane is formed once here instead
@@ -524,9 +585,15 @@ class DeviceSolver:
         else:
             ws.z.copy_(dev.to_device(Y0, self.device))
 
-        t0 = time.perf_counter()
+        # device time between events on the solver stream: work queued before the
+        # solve (e.g. the generalized forward map) is not charged to Lanczos
+        e_l0 = torch.cuda.Event(enable_timing=True)
+        e_l1 = torch.cuda.Event(enable_timing=True)
+        e_l0.record(self.eng.stream)
         b_up = _lanczos(self.hm, cfg.lanczos_steps, rng)
-        report.t_lanczos = time.perf_counter() - t0
+        e_l1.record(self.eng.stream)
+        e_l1.synchronize()
+        report.t_lanczos = e_l0.elapsed_time(e_l1) * 1e-3
         report.setup_matmuls += min(cfg.lanczos_steps, n)
         report.upper_bound = b_up
 
@@ -534,15 +601,17 @@ class DeviceSolver:
             lam_ref, a_edge = float(prior[0]), float(prior[1])
         else:
             # bootstrap: one unfiltered Rayleigh-Ritz pass on the start block
-            t0 = time.perf_counter()
+            e_l0.record(self.eng.stream)
             q = self._orthonormalize(ws.z, None, ws.hq, ws.fa, rng)
             if self.sharded is not None:
                 w, _, wvec = self.sharded.rayleigh_ritz(self.eng, self.hb, q, ws.hq, ws.fb, ws.hz)
                 self.sharded.ritz_columns(self.eng, q, wvec, 0, None, ws.z)
             else:
                 w = self.eng.rayleigh_ritz(self.hb, q, ws.hq, ws.z, ws.hz)
+            e_l1.record(self.eng.stream)
+            e_l1.synchronize()
             _count_products(s_tot)
-            report.t_rr += time.perf_counter() - t0
+            report.t_rr += e_l0.elapsed_time(e_l1) * 1e-3
             report.setup_matmuls += s_tot
             lam_ref, a_edge = float(w[0]), float(w[nev])
             if cfg.interval == "block_top":
@@ -561,32 +630,9 @@ class DeviceSolver:
                 b_up = a_edge + max(1.0, abs(a_edge)) * 1e-8
             ncols = dev.cols(act)
 
-            # phase times from CUDA events on the solver stream: the iteration needs
-            # only two host syncs (rank test after CholQR2; Ritz values + residuals)
-            locked = ws.locked[:nl] if nl else None
-            ev[0].record(self.eng.stream)
-            f = self._filter(act, ws.fb[:ncols], a_edge, b_up, lam_ref, locked)
-            ev[1].record(self.eng.stream)
-            _count_products(cfg.degree * ncols)
+            q, w, res, wvec, tf, tq, trr = self._phases(act, ws, nl, a_edge, b_up, lam_ref,
+                                                        rng, ev)
             report.filter_flops += 8.0 * n * n * cfg.degree * ncols
-
-            q = self._orthonormalize(f, locked, ws.hq[:ncols], ws.fa[:ncols], rng,
-                                     projected=self.sharded is not None)
-            ev[2].record(self.eng.stream)
-
-            if self.sharded is not None:
-                # f (in ws.fb) is dead after the QR: its buffer takes the own Ritz vectors
-                w, res, wvec = self.sharded.rayleigh_ritz(self.eng, self.hb, q, ws.hq[:ncols],
-                                                          ws.fb[:ncols], ws.hz[:ncols])
-            else:
-                w, res = self.eng.rayleigh_ritz(self.hb, q, ws.hq[:ncols], ws.z[:ncols],
-                                                ws.hz[:ncols], residuals=True)
-            ev[3].record(self.eng.stream)
-            _count_products(ncols)
-            ev[3].synchronize()
-            tf = ev[0].elapsed_time(ev[1]) * 1e-3
-            tq = ev[1].elapsed_time(ev[2]) * 1e-3
-            trr = ev[2].elapsed_time(ev[3]) * 1e-3  # includes the fused residual norms
             tres = 0.0
 
             kk = 0
@@ -637,14 +683,16 @@ class DeviceSolver:
                 VectorBlock(vecs.clone()) if nl else dev.to_host(vecs), report)
 
         vals = np.asarray(locked_vals)
-        t0 = time.perf_counter()
+        e_l0.record(self.eng.stream)
         if self.sharded is not None:
             final_res = self.sharded.residual_check(self.eng, self.hb, vecs, vals, ws.hq[:nev])
         else:
             self.eng.apply_operator(self.hb, vecs, ws.hq[:nev])
             final_res = self.eng.residual_norms(ws.hq[:nev], vecs, vals)
+        e_l1.record(self.eng.stream)
+        e_l1.synchronize()
         _count_products(nev)
-        report.t_resid += time.perf_counter() - t0
+        report.t_resid += e_l0.elapsed_time(e_l1) * 1e-3
         report.total_matmuls += nev
         report.t_total = time.perf_counter() - t_start
         out = vecs.clone()
@@ -684,6 +732,11 @@ def _localize(x, memo=None):
     return out
 
 
+def _default_devices():
+    from .comm import default_devices
+    return default_devices()
+
+
 def _in_process(devices, group, fn, seed):
     """Run ``fn(comm, seed_copy)`` on one thread per GPU of ``devices`` (comm.py) and
     return rank 0's result. Every rank gets its own copy of the caller's Generator (the
@@ -696,7 +749,8 @@ def _in_process(devices, group, fn, seed):
     devs = normalize_devices(devices)
     rngs = [clone_rng(seed) for _ in devs]
     if len(devs) == 1:
-        with torch.cuda.device(devs[0]):
+        from .comm import inside_group
+        with torch.cuda.device(devs[0]), inside_group():
             out = fn(None, rngs[0])
     else:
         out = run_on_devices(devs, lambda comm: fn(comm, rngs[comm.rank]))[0]
@@ -718,6 +772,8 @@ def chfsi_solve(H, Y0, config, prior=None, seed=0, *, group=None, devices=None,
     an NCCL clique (comm.py); results on the first device.
     ``callback`` (keyword-only, B200 extension): called with each IterationStat.
     """
+    if devices is None and group is None:
+        devices = _default_devices()
     if devices is not None:
         return _in_process(devices, group, lambda comm, rng: chfsi_solve(
             _localize(H), _localize(Y0), config, prior, rng, group=comm,
@@ -757,6 +813,8 @@ def solve_generalized(A, B, Y0, config, prior=None, seed=0, *, group=None, devic
     B = L L^H (cuSOLVER zpotrf), H = L^-1 A L^-H (triangular inverse + DMMA
     GEMMs), ChFSI on H, C = L^-H Y. Returns B-orthonormal vectors.
     ``group`` / ``devices``: as for chfsi_solve."""
+    if devices is None and group is None:
+        devices = _default_devices()
     if devices is not None:
         return _in_process(devices, group, lambda comm, rng: solve_generalized(
             _localize(A), _localize(B), _localize(Y0), config, prior, rng, group=comm,

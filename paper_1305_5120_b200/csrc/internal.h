@@ -43,7 +43,7 @@ struct Handle {
   cudaStream_t stream = nullptr;
   cusolverDnHandle_t solver = nullptr;
   // grow-only scratch arenas (stream-ordered reuse is safe: one stream)
-  static constexpr int kSlots = 11;
+  static constexpr int kSlots = 12;
   void* scratch[kSlots] = {nullptr};
   size_t scratch_bytes[kSlots] = {0};
   int* d_info = nullptr;
@@ -84,6 +84,7 @@ enum Slot : int {
   SLOT_COLRED = 8,  // per-column partial sums (split column reductions)
   SLOT_HSUM = 9,    // 3M sum plane of the filter operator H (n x n doubles)
   SLOT_YSUM = 10,   // 3M sum planes of the two rotating filter blocks (2 x n x k doubles)
+  SLOT_GEMV = 11,   // column-split partial products of the HBM-bound GEMV
 };
 
 void set_error(const std::string& msg);
@@ -182,6 +183,11 @@ int trtri_lower(Handle* h, long long n, const double2* L, long long ldl, double2
 int zaxpby_cols(Handle* h, long long n, long long k, double2 alpha, const double2* X,
                 long long ldx, double2 beta, double2* Y, long long ldy);
 int get_real_diag(Handle* h, long long n, const double2* A, long long lda, double* out_dev);
+// y = alpha A x + beta y for a column-major M x K matrix A (HBM-bound GEMV; the
+// Lanczos H v of core.py:202-256): one row per thread, the K columns split over
+// blockIdx.y, partial products summed in fixed order (deterministic).
+int zgemv_n(Handle* h, long long M, long long K, double2 alpha, const double2* A, long long lda,
+            const double2* x, double2 beta, double2* y);
 int zcopy2d(Handle* h, long long rows, long long cols, const double2* src, long long lds,
             double2* dst, long long ldd);
 int shift_diag(Handle* h, long long n, double2* A, long long lda, double shift);

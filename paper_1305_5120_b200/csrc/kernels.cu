@@ -99,6 +99,72 @@ __global__ void zdotc_partial_kernel(long long n, int S, const double2* __restri
   if (threadIdx.x == 0) partial[j * S + s] = make_double2(sr, si);
 }
 
+// GEMV y = alpha A x + beta y, A column-major M x K (the Lanczos H v, core.py:202-256):
+// HBM-bound (16 bytes of A per complex MAC). Thread r of the grid owns row r, so each
+// column of A is read by consecutive threads (coalesced 512-byte warp segments) with
+// streaming loads (A is read once); every thread keeps GV_U independent loads in
+// flight. The K columns are split over blockIdx.y (S chunks) so the grid holds
+// enough loads in flight to saturate HBM even for one column; the S partial rows are
+// summed in fixed order by zgemv_finish_kernel (deterministic, no atomics).
+constexpr int GV_T = 256;
+constexpr int GV_U = 8;
+
+__global__ void __launch_bounds__(GV_T) zgemv_partial_kernel(long long M, long long K, int S,
+                                                             const double2* __restrict__ A,
+                                                             long long lda,
+                                                             const double2* __restrict__ x,
+                                                             double2* __restrict__ partial) {
+  const long long r = (long long)blockIdx.x * GV_T + threadIdx.x;
+  const int s = blockIdx.y;
+  const long long chunk = (K + S - 1) / S;
+  const long long c0 = s * chunk, c1 = min(K, c0 + chunk);
+  if (r >= M) return;
+  const double2* a = A + r;
+  double ar = 0.0, ai = 0.0;
+  long long c = c0;
+  for (; c + GV_U <= c1; c += GV_U) {
+    double2 hv[GV_U];
+    #pragma unroll
+    for (int u = 0; u < GV_U; ++u) hv[u] = __ldcs(a + (c + u) * lda);
+    #pragma unroll
+    for (int u = 0; u < GV_U; ++u) {
+      const double2 xv = __ldg(x + c + u);
+      ar = fma(hv[u].x, xv.x, ar);
+      ar = fma(-hv[u].y, xv.y, ar);
+      ai = fma(hv[u].x, xv.y, ai);
+      ai = fma(hv[u].y, xv.x, ai);
+    }
+  }
+  for (; c < c1; ++c) {
+    const double2 hv = __ldcs(a + c * lda);
+    const double2 xv = __ldg(x + c);
+    ar = fma(hv.x, xv.x, ar);
+    ar = fma(-hv.y, xv.y, ar);
+    ai = fma(hv.x, xv.y, ai);
+    ai = fma(hv.y, xv.x, ai);
+  }
+  partial[(long long)s * M + r] = make_double2(ar, ai);
+}
+
+__global__ void zgemv_finish_kernel(long long M, int S, const double2* __restrict__ partial,
+                                    double2 alpha, double2 beta, double2* __restrict__ y) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  double sr = 0.0, si = 0.0;
+  for (int t = 0; t < S; ++t) {
+    const double2 p = partial[(long long)t * M + r];
+    sr += p.x;
+    si += p.y;
+  }
+  double2 out = make_double2(alpha.x * sr - alpha.y * si, alpha.x * si + alpha.y * sr);
+  if (beta.x != 0.0 || beta.y != 0.0) {
+    const double2 o = y[r];
+    out.x += beta.x * o.x - beta.y * o.y;
+    out.y += beta.x * o.y + beta.y * o.x;
+  }
+  y[r] = out;
+}
+
 __global__ void finish_sqrt_kernel(long long k, int S, const double* __restrict__ partial,
                                    double* __restrict__ out) {
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -512,6 +578,28 @@ int get_real_diag(Handle* h, long long n, const double2* A, long long lda, doubl
 
 int shift_diag(Handle* h, long long n, double2* A, long long lda, double shift) {
   shift_diag_kernel<<<grid_for(n), 256, 0, h->stream>>>(n, A, lda, shift);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  return OK;
+}
+
+int zgemv_n(Handle* h, long long M, long long K, double2 alpha, const double2* A, long long lda,
+            const double2* x, double2 beta, double2* y) {
+  if (M <= 0) return OK;
+  const long long bx = (M + GV_T - 1) / GV_T;
+  // ~8 resident 256-thread CTAs per SM (full occupancy) over the whole grid
+  const long long want = 8LL * h->sm_count;
+  long long S = std::max<long long>(1, (want + bx - 1) / bx);
+  S = std::min<long long>(S, std::max<long long>(1, K / (4 * GV_U)));
+  S = std::min<long long>(S, 64);
+  double2* part = (double2*)scratch(h, SLOT_GEMV, (size_t)S * M * sizeof(double2));
+  if (!part) return ERR_NOMEM;
+  zgemv_partial_kernel<<<dim3((unsigned)bx, (unsigned)S), GV_T, 0, h->stream>>>(M, K, (int)S, A,
+                                                                              lda, x, part);
+  h->launches++;
+  CHFSI_CHECK_LAUNCH();
+  zgemv_finish_kernel<<<(unsigned)((M + 255) / 256), 256, 0, h->stream>>>(M, (int)S, part, alpha,
+                                                                          beta, y);
   h->launches++;
   CHFSI_CHECK_LAUNCH();
   return OK;

@@ -738,6 +738,11 @@ int zgemm(Handle* h, int opa, int opb, long long M, long long N, long long K, do
   }
   p.tri = tri;
   p.tri_off = (int)tri_off;
+  // a matrix-vector product is HBM-bound: a dedicated GEMV instead of padding the one
+  // column to an 8-wide tensor-core tile (the Lanczos H v)
+  if (N == 1 && opa == OP_N && opb == OP_N && tri == 0 && M >= 256 && K >= 1 &&
+      g_force_cfg < 0)
+    return zgemv_n(h, M, K, alpha, A, lda, B, beta, C);
   return launch(h, opa, opb, EPI_STORE, M, N, K, p);
 }
 

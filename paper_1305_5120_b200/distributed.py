@@ -142,6 +142,10 @@ def check_agreement(extras, what):
                          f"consistently")
 
 
+# test-only fault injection (tests/test_multigpu.py): "perturb_gram" -> (rank, fn(G))
+TEST_HOOKS = {}
+
+
 class ShardedPhases:
     """Column-sharded phases of one outer iteration.
 
@@ -172,7 +176,7 @@ class ShardedPhases:
         self._bufs = {}
         self._weights = None
         # test hook: (rank, callable(G)) applied to that rank's gathered RR Gram
-        self._perturb_gram = None
+        self._perturb_gram = TEST_HOOKS.get("perturb_gram")
 
     def agree(self, what, values, like):
         """Cross-rank consistency guard for the replicated k x k decisions (Cholesky

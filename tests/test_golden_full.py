@@ -1,0 +1,102 @@
+"""Full-size parity against the REFERENCE itself (north_star:
+eigenvalues within 1e-10 relative, residuals below tol, the same number of converged
+pairs, largest principal angle < 1e-8).
+
+Fixtures (scripts/make_golden.py --c1 / --c2p1, written by running the unmodified
+reference /root/reference/pkg/src/chfsi in the build container):
+
+* tests/golden/c1_full.npz -- BASELINE config 1 in full: 5 correlated n = 2000
+  problems through the reference's solve_sequence (sequence.py:165-228), reuse mode,
+  nev = 200, nex = 40, m = 20, tol 1e-10 (about 20 min of CPU on 8 cores).
+* tests/golden/c2p1_full.npz -- BASELINE config 2, problem 1: generalized n = 5000,
+  nev = 500, nex = 50, m = 20 (reference solve_generalized via solve_sequence).
+
+The n x nev eigenvector blocks are not stored; a subspace sketch is: P Z with P the
+orthogonal projector onto span(V) and Z a seeded n x 8 complex Gaussian probe.
+||P_gpu Z - P_ref Z||_F / sqrt(2 p) estimates ||P_gpu - P_ref||_F / sqrt(2) =
+sqrt(sum_i sin^2 theta_i) >= sin(theta_max), so bounding it by 1e-8 is at least as
+strict as the north star's largest-angle bar (up to the probe's sampling error).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _sketch(v, seed, p=8):
+    q, _ = np.linalg.qr(v)
+    z = np.random.default_rng(int(seed))
+    z = z.standard_normal((v.shape[0], p)) + 1j * z.standard_normal((v.shape[0], p))
+    return q @ (q.conj().T @ z)
+
+
+def _sketch_angle(v, ref_sketch, seed):
+    p = ref_sketch.shape[1]
+    return float(np.linalg.norm(_sketch(v, seed, p) - ref_sketch) / np.sqrt(2.0 * p))
+
+
+def _load(name):
+    path = os.path.join(GOLD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated (scripts/make_golden.py)")
+    return np.load(path)
+
+
+def test_c1_full_sequence_matches_reference():
+    """BASELINE c1 in full through solve_sequence: per cycle the eigenvalues, the
+    converged count, the subspace (sketch) and the outer-iteration count (+-2 %) match
+    the reference's own run."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    g = _load("c1_full.npz")
+    # the same recipe and seeds as the reference's run (bit-identical only with the same
+    # host BLAS: the fixture's h_sha pins the build box's matrices; a different CPU's
+    # OpenBLAS kernels change the last bits of the QR/products, far below the 1e-10 bar)
+    probs = baseline_sequence(0, 2000, 5)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=2000, N=5, nev=200, seed=0),
+                            problems=[(a, None) for a, _ in probs])
+    cfg = G.SolverConfig(nev=200, buffer=40, degree=20, max_outer_iters=20000)
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
+    seed = int(g["probe_seed"])
+    for i in range(5):
+        lam_ref = g[f"lam{i}"]
+        lam = rep.eigenvalues[i]
+        assert len(lam) == len(lam_ref) == 200
+        assert np.max(np.abs(lam - lam_ref) / np.abs(lam_ref)) <= 1e-10, i
+        v = rep.vectors[i].entries
+        assert np.max(G.residuals(probs[i][0], v, lam)) < cfg.tol
+        assert _sketch_angle(v, g[f"sketch{i}"], seed) < 1e-8, i
+        n_ref = len(g[f"it_filtered{i}"])
+        assert abs(rep.reports[i].outer_iterations - n_ref) <= max(2, 0.02 * n_ref), \
+            (i, rep.reports[i].outer_iterations, n_ref)
+
+
+def test_c2_problem1_generalized_matches_reference():
+    """BASELINE c2 problem 1 (generalized, n = 5000, nev = 500) against the reference:
+    eigenvalues, converged count, B-orthonormality, generalized residuals, the subspace
+    sketch and the iteration count (+-2 %)."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    g = _load("c2p1_full.npz")
+    (a, s), = baseline_sequence(0, 5000, 1, generalized=True)  # (see the c1 note on h_sha)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=5000, N=1, nev=500, seed=0,
+                                                kind="generalized"),
+                            problems=[(a, s)])
+    cfg = G.SolverConfig(nev=500, buffer=50, degree=20, max_outer_iters=20000)
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
+    lam, c = rep.eigenvalues[0], rep.vectors[0].entries
+    lam_ref = g["lam"]
+    assert len(lam) == len(lam_ref) == 500
+    assert np.max(np.abs(lam - lam_ref) / np.abs(lam_ref)) <= 1e-10
+    assert np.linalg.norm(c.conj().T @ s @ c - np.eye(500)) <= 1e-9
+    res = np.linalg.norm(a @ c - (s @ c) * lam, axis=0)
+    assert np.max(res) <= cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(s, 1))
+    assert _sketch_angle(c, g["sketch"], int(g["probe_seed"])) < 1e-8
+    n_ref = len(g["it_filtered"])
+    assert abs(rep.reports[0].outer_iterations - n_ref) <= max(2, 0.02 * n_ref), \
+        (rep.reports[0].outer_iterations, n_ref)

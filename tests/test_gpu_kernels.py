@@ -761,3 +761,67 @@ def test_project_out_and_rr_from_hq(eng):
     w2, r2 = eng.rayleigh_ritz_from_hq(dQ, bufs[3], bufs[4], bufs[5])
     assert np.array_equal(w1, w2) and np.array_equal(r1, r2)
     assert np.array_equal(D.to_host(bufs[1]), D.to_host(bufs[4]))
+
+
+@pytest.mark.parametrize("off", [3, 8, 13])
+@pytest.mark.parametrize("split", [0, 3])
+def test_zgemm_tri_offsets_and_split(eng, off, split):
+    """chfsi_zgemm_tri with every triangular flag at shard offsets that are and are not
+    multiples of the 8-column K tile, auto and forced split-K: the TMA kernels load whole
+    K tiles and cannot mask a triangular bound inside one, so unaligned offsets plan onto
+    the element-masked kernels (a tile straddling two split-K chunks would otherwise be
+    counted twice). Against numpy on factors whose zero triangle holds zeros."""
+    from paper_1305_5120_b200 import _native, device as D
+    lib = _native.load()
+    rng = np.random.default_rng(900 + off + split)
+    K, M, N = 600, 45, 37
+    L = np.tril(crand(rng, K, K))
+    X = crand(rng, K, 29)
+    Y = crand(rng, 31, K)
+    cases = [
+        # (flag, opa, opb, A, B, m, n, reference)
+        (eng.TRI_B_LOWER, "N", "N", Y, L[:, off:off + N], 31, N, Y @ L[:, off:off + N]),
+        (eng.TRI_A_LOWER, "N", "N", L[off:off + M, :], X, M, 29, L[off:off + M, :] @ X),
+        (eng.TRI_B_UPPER, "N", "C", Y, L[off:off + N, :], 31, N, Y @ L[off:off + N, :].conj().T),
+        (eng.TRI_A_UPPER, "C", "N", L[:, off:off + M], X, M, 29, L[:, off:off + M].conj().T @ X),
+    ]
+    try:
+        assert lib.chfsi_gemm_override(-1, split) == 0
+        for flag, opa, opb, A, B, m, n, ref in cases:
+            dC = D.zeros(m, n, eng.device)
+            eng.zgemm(opa, opb, m, n, K, 1.0, D.to_device(A, eng.device),
+                      D.to_device(B, eng.device), 0.0, dC, tri=flag, tri_offset=off)
+            got = D.to_host(dC)
+            assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref), (flag, off, split)
+    finally:
+        lib.chfsi_gemm_override(-1, 0)
+
+
+@pytest.mark.parametrize("m,k,pad", [(256, 256, 0), (300, 1000, 5), (5003, 4001, 13), (20000, 64, 0)])
+def test_zgemv_hbm_path(eng, m, k, pad):
+    """Matrix-vector products (N = 1, op N x N: the Lanczos H v) take the HBM-bound GEMV
+    (row per thread, column-split partials summed in fixed order): alpha/beta, a padded
+    leading dimension, bit-identical repeats, against numpy."""
+    import torch
+    from paper_1305_5120_b200 import device as D
+    rng = np.random.default_rng(m + k + pad)
+    A = crand(rng, m, k)
+    x = crand(rng, k, 1)
+    y0 = crand(rng, m, 1)
+    dA_full = D.zeros(m + pad, k, eng.device)
+    dA_full[:, :m].copy_(torch.from_numpy(np.ascontiguousarray(A.T)).to(eng.device))
+    dA = dA_full[:, :m] if pad else dA_full
+    al, be = 0.6 + 0.3j, -0.25 + 0.1j
+    outs = []
+    for _ in range(2):
+        dy = D.to_device(y0, eng.device)
+        eng.zgemm("N", "N", m, 1, k, al, dA, D.to_device(x, eng.device), be, dy)
+        outs.append(D.to_host(dy))
+    ref = al * (A @ x) + be * y0
+    assert np.array_equal(outs[0], outs[1])
+    assert np.linalg.norm(outs[0] - ref) <= 1e-14 * np.linalg.norm(ref) * np.sqrt(k)
+    n0 = eng.launch_count(reset=True)
+    dy = D.to_device(y0, eng.device)
+    eng.zgemm("N", "N", m, 1, k, 1.0, dA, D.to_device(x, eng.device), 0.0, dy)
+    assert eng.launch_count(reset=True) == 2  # partial + fixed-order finish
+    del n0
