@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--block-cols", dest="k", type=int, default=2200)
     ap.add_argument("--degree", type=int, default=25)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/tail/solve legs")
+    ap.add_argument("--legs", default="",
+                    help="comma list: run only these extra legs (development; default all)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--complex-mul", type=int, default=3, choices=[3, 4],
                     help="complex products of the GEMMs: 3 (3M, default) or 4 real DMMA "
@@ -65,6 +67,11 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: host-staged, for testing)")
     return ap.parse_args()
+
+
+def want(args, key):
+    """Extra legs to run: all by default, or the --legs subset."""
+    return not args.legs or key in args.legs.split(",")
 
 
 def workload_cfg(args, n_gpus):
@@ -337,7 +344,7 @@ def run_b200(args, rank, world, local_rank):
 
     kernel_name = plan_kernel_name(eng, n, kp)
     e2e_multi = None
-    if world > 1 and not args.no_extras:
+    if world > 1 and not args.no_extras and want(args, "e2e"):
         # every rank takes part (collectives inside); max over ranks
         e2e_multi = e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up,
                                     lam_ref, dev)
@@ -351,11 +358,14 @@ def run_b200(args, rank, world, local_rank):
         if not args.no_extras:
             # s per ChFSI solve at the metric's n on all ranks (column-sharded)
             nev_s = int(round(k * 2000 / 2200))
-            solve = guarded_leg(line, rank, lambda: solve_c4_leg(H, lam, rank, world, dev,
-                                                                 nev_s, k - nev_s, m))
-            if rank == 0:
-                line["solve_c4"] = solve
+            if want(args, "solve_c4"):
+                solve = guarded_leg(line, rank, lambda: solve_c4_leg(H, lam, rank, world, dev,
+                                                                     nev_s, k - nev_s, m))
+                if rank == 0:
+                    line["solve_c4"] = solve
             for key, fn in extra_solve_legs(H, lam, rank, world, dev, nev_s, k - nev_s, m):
+                if not want(args, key):
+                    continue
                 out = guarded_leg(line, rank, fn, key=key)
                 if rank == 0:
                     line[key] = out
@@ -400,6 +410,8 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
     if not args.no_extras:
         def leg(key, fn):
             # an optional leg must never cost the headline line
+            if not want(args, key):
+                return
             try:
                 line[key] = fn()
             except Exception as exc:  # pragma: no cover - reported, not raised
@@ -407,6 +419,8 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
             torch.cuda.empty_cache()
 
         leg("e2e", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev))
+        leg("e2e_pageable", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev,
+                                            pinned=False))
         leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
         other = 4 if args.complex_mul == 3 else 3
         leg(f"filter_complex_mul_{other}",
@@ -417,11 +431,13 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
         del Yfull, Y0, Y, W
         torch.cuda.empty_cache()
         nev_s = int(round(args.k * 2000 / 2200))
-        line["solve_c4"] = guarded_leg(line, 0, lambda: solve_c4_leg(
-            H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree))
+        if want(args, "solve_c4"):
+            line["solve_c4"] = guarded_leg(line, 0, lambda: solve_c4_leg(
+                H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree))
         for key, fn in extra_solve_legs(H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree):
-            line[key] = guarded_leg(line, 0, fn, key=key)
-            torch.cuda.empty_cache()
+            if want(args, key):
+                line[key] = guarded_leg(line, 0, fn, key=key)
+                torch.cuda.empty_cache()
         del H
         torch.cuda.empty_cache()
         leg("solve_c0", solve_c0)
@@ -833,17 +849,20 @@ def e2e_leg_sharded(args, H, Yfull, shards, rank, world, a_edge, b_up, lam_ref, 
                     "rank 0 VectorBlock -> host"}
 
 
-def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
-    """Same filter through the public API with pinned host inputs; H2D/D2H inside."""
+def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2, pinned=True):
+    """Same filter through the public API with host inputs; H2D/D2H inside. pinned=True:
+    page-locked host H / Y; pinned=False: plain (pageable) numpy arrays, as a drop-in
+    caller of the reference's chebyshev_filter passes them (core.py:287-311) -- the
+    library stages them through its pinned ring (csrc/staging.cu)."""
     import torch
 
     import paper_1305_5120_b200 as G
     n, k, m = args.n, args.k, args.degree
-    h_pin = torch.empty((n, n), dtype=torch.complex128, pin_memory=True)
+    h_pin = torch.empty((n, n), dtype=torch.complex128, pin_memory=pinned)
     h_pin.copy_(H)
-    y_pin = torch.empty((k, n), dtype=torch.complex128, pin_memory=True)
+    y_pin = torch.empty((k, n), dtype=torch.complex128, pin_memory=pinned)
     y_pin.copy_(Yfull)
-    h_np = h_pin.numpy().T  # F-order n x n view of the pinned buffer (column j = row j)
+    h_np = h_pin.numpy().T  # F-order n x n view of the host buffer (column j = row j)
     y_np = y_pin.numpy().T
     spec = G.FilterSpec(degree=m, a=a_edge, b=b_up, lam_ref=lam_ref)
     out = G.chebyshev_filter(h_np, y_np, spec)  # warm-up
@@ -868,6 +887,7 @@ def e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev, steps=2):
     return {"value": flops * steps / dt / 1e12, "unit": UNIT,
             "h2d_bytes_per_step": int(16 * n * n + 16 * n * k),
             "d2h_bytes_per_step": nbytes, "steps": steps, "results_finite": all(checks),
+            "host_memory": "page-locked" if pinned else "pageable numpy (staged by the library)",
             "path": "paper_1305_5120_b200.chebyshev_filter(H, Y, FilterSpec) -> VectorBlock.entries"}
 
 

@@ -228,6 +228,17 @@ int chfsi_apply_operator(chfsi_handle_t h, int64_t n, int64_t k, const void* d_H
 int chfsi_peak_dmma(int device, int iters, double* h_tflops);
 int chfsi_peak_dfma(int device, int iters, double* h_tflops);
 
+/* Upload a rows x cols column-major complex block from host memory (ld_src) to the
+ * device (ld_dst) on the handle's stream -- the H2D half of every drop-in call that
+ * passes numpy arrays (core.py:287-311, :385; linalg.py:89-93 `_asarray`). Page-locked
+ * sources take one async 2-D copy; pageable ones go through the handle's pinned staging
+ * ring, filled by a host worker pool while the DMA engine drains the previous slot
+ * (CHFSI_STAGE_MB per slot, CHFSI_STAGE_THREADS workers). Returns once the source has
+ * been read; the device copy completes in stream order. chfsi_filter_streamed uses the
+ * same path for the panels of a pageable H. */
+int chfsi_upload(chfsi_handle_t h, const void* h_src, int64_t ld_src, int64_t rows,
+                 int64_t cols, void* d_dst, int64_t ld_dst);
+
 /* In-process multi-GPU (SURVEY.md section 8b `chfsi_ctx_create(ndev, devices)`): one
  * NCCL clique over `ndev` distinct GPUs of this process (ncclCommInitAll), one rank per
  * device, each driven by its own host thread. The reference takes its parallelism

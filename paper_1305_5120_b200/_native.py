@@ -86,6 +86,7 @@ SIGNATURES = {
     "chfsi_gemm_plan": (_int, [_c_void_p, _int, _int, _int, _i64, _i64, _i64, _pint, _pint]),
     "chfsi_peak_dmma": (_int, [_int, _int, _pdbl]),
     "chfsi_peak_dfma": (_int, [_int, _int, _pdbl]),
+    "chfsi_upload": (_int, [_c_void_p, _c_void_p, _i64, _i64, _i64, _c_void_p, _i64]),
     "chfsi_comm_available": (_int, [_pint]),
     "chfsi_comm_init_all": (_int, [_int, _pint, ctypes.POINTER(_c_void_p)]),
     "chfsi_comm_destroy": (_int, [_c_void_p]),

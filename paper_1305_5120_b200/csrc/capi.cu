@@ -209,6 +209,7 @@ int chfsi_destroy(chfsi_handle_t h) {
   cudaStreamSynchronize(h->stream);
   destroy_filter_graphs(h);
   destroy_copy_stream(h);
+  destroy_stager(h);
   if (h->capture_stream) cudaStreamDestroy(h->capture_stream);
   for (int i = 0; i < Handle::kSlots; ++i)
     if (h->scratch[i]) cudaFree(h->scratch[i]);
@@ -275,6 +276,21 @@ int chfsi_filter(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a, d
   }
   return filter(h, n, k, degree, a, b, lam_ref, (const double2*)d_H, ldh, (double2*)d_Y, ldy,
                 (double2*)d_W, ldw, h_result_in_w);
+}
+
+int chfsi_upload(chfsi_handle_t h, const void* h_src, int64_t ld_src, int64_t rows,
+                 int64_t cols, void* d_dst, int64_t ld_dst) {
+  H_CHECK(h);
+  if ((!h_src || !d_dst) && rows > 0 && cols > 0) {
+    set_error("chfsi_upload: null pointer");
+    return ERR_ARG;
+  }
+  CHFSI_TRY(upload_2d(h, (const double2*)h_src, ld_src, rows, cols, (double2*)d_dst, ld_dst,
+                      h->stream));
+  // a page-locked source is read by the DMA engine asynchronously: return only once it
+  // has been, so the caller may free or overwrite it (the staged path already has)
+  if (host_is_pinned(h_src)) CHFSI_CUDA(cudaStreamSynchronize(h->stream));
+  return OK;
 }
 
 int chfsi_filter_streamed(chfsi_handle_t h, int64_t n, int64_t k, int degree, double a,

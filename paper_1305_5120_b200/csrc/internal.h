@@ -66,10 +66,21 @@ struct Handle {
   // host->device upload stream and its per-panel events (streamed filter)
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t>* copy_events = nullptr;
+  // pinned staging ring + host worker pool for pageable uploads (staging.cu)
+  struct Stager* stager = nullptr;
 };
 
 void destroy_filter_graphs(Handle* h);
 void destroy_copy_stream(Handle* h);
+void destroy_stager(Handle* h);
+
+// rows x cols column-major host block (ld_host, complex) -> device (ld_dev) on `stream`.
+// Pinned sources: one async 2-D copy. Pageable sources: through the handle's pinned
+// staging ring (host worker threads fill a slot while the DMA drains the previous one);
+// returns once the host source has been read.
+int upload_2d(Handle* h, const double2* host, long long ld_host, long long rows,
+              long long cols, double2* dev, long long ld_dev, cudaStream_t stream);
+bool host_is_pinned(const void* p);
 
 // scratch slots
 enum Slot : int {

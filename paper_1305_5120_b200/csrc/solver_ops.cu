@@ -298,9 +298,9 @@ int filter_streamed(Handle* h, long long n, long long k, int degree, double a, d
   for (int p = 0; p < panels; ++p) {
     const long long r0 = p * rows;
     const long long m = std::min(rows, n - r0);
-    CHFSI_CUDA(cudaMemcpy2DAsync(H + r0, (size_t)ldh * sizeof(double2), H_host + r0,
-                                 (size_t)ldh_host * sizeof(double2), (size_t)m * sizeof(double2),
-                                 (size_t)n, cudaMemcpyHostToDevice, h->copy_stream));
+    // pinned: one strided 2-D copy; pageable: through the pinned staging ring, the host
+    // threads filling panel p + 1 while panel p's step runs (staging.cu)
+    CHFSI_TRY(upload_2d(h, H_host + r0, ldh_host, m, n, H + r0, ldh, h->copy_stream));
     CHFSI_CUDA(cudaEventRecord(ev[p], h->copy_stream));
     // enqueue the panel's step right behind its copy: with pageable host memory the
     // copy call returns only once staged, and the step of panel p then overlaps the

@@ -72,12 +72,25 @@ def zeros(n, k, device):
     return torch.zeros((k, n), dtype=CDT, device=device)
 
 
+# pageable host blocks at least this large go through the native staged upload
+_STAGED_MIN_BYTES = 8 << 20
+
+
 def to_device(arr, device, pin=False):
-    """numpy (n,) / (n, k) complex array -> device tensor (k, n) (column-major block)."""
+    """numpy (n,) / (n, k) complex array -> device tensor (k, n) (column-major block).
+    Large pageable arrays are uploaded by chfsi_upload (pinned staging ring filled by
+    host worker threads, csrc/staging.cu) instead of the driver's pageable path."""
     a = np.asarray(arr, dtype=np.complex128)
     if a.ndim == 1:
         a = a.reshape(-1, 1)
     a = np.asfortranarray(a)
+    if (not pin and a.nbytes >= _STAGED_MIN_BYTES and a.size
+            and torch.device(device).type == "cuda"):
+        out = torch.empty((a.shape[1], a.shape[0]), dtype=CDT, device=device)
+        eng = Engine.get(out.device)
+        _native.call("chfsi_upload", eng.h, ctypes.c_void_p(a.ctypes.data), a.shape[0],
+                     a.shape[0], a.shape[1], ctypes.c_void_p(out.data_ptr()), a.shape[0])
+        return out
     with warnings.catch_warnings():
         # read-only inputs (frozen VectorBlock.entries) are only read by the H2D copy
         warnings.filterwarnings("ignore", message="The given NumPy array is not writable")

@@ -44,7 +44,7 @@ def interp(table, k):
 def main():
     solve = json.load(open(sys.argv[1]))
     kxk = {int(k): v for k, v in json.load(open(sys.argv[2])).items()}
-    tune_path = sys.argv[3] if len(sys.argv) > 3 else "profiles/r01/tune_sweep_filter_after.json"
+    tune_path = sys.argv[3] if len(sys.argv) > 3 else "profiles/r01/filter_widths_3m.json"
     step = {r["k"]: r["ms"] * 1e-3 for r in json.load(open(tune_path))
             if r["cfg"] == -1 and r["n"] == N_ORDER}
     chol = {k: v["chol_inv_s"] for k, v in kxk.items()}
