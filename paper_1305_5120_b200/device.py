@@ -34,7 +34,9 @@ def cols(t):
 def _check_layout(t):
     """A (k, n) block must be column-major: unit stride along rows (the kernels read
     column j at data_ptr + j * ld) and ld >= n; a transposed or strided view would be
-    read with the wrong layout."""
+    read with the wrong layout. Empty blocks are not read (their strides are arbitrary)."""
+    if t.numel() == 0:
+        return
     if t.dim() == 2 and t.shape[1] > 1 and t.stride(1) != 1:
         raise ValueError(f"block has row stride {t.stride(1)}; the kernels need unit stride "
                          f"along rows (a (cols, rows) tensor with contiguous columns)")
