@@ -3,6 +3,11 @@
 
     python scripts/scaling_model.py SOLVE.json KXK.json [TUNE.json]
 
+    e.g. SOLVE.json = profiles/r01/solves/c4_standard_problem1_block_top_3m.json
+         (block_top) or ..._reference_interval_3m.json (the reference's semantics);
+         KXK.json = profiles/r01/kxk_probe.json; TUNE.json defaults to the 3M
+         per-width table profiles/r01/filter_widths_3m.json.
+
 Inputs, all measured on one B200:
   SOLVE.json  scripts/c4_solve.py output with per-iteration phase times
               [cols, locked, t_filter, t_qr, t_rr] (1 GPU);
@@ -57,6 +62,11 @@ def main():
     print(f"1 GPU: {t1:.1f} s ({len(its)} iterations; filter {p['t_filter']:.1f}, "
           f"QR {p['t_qr']:.2f}, RR {p['t_rr']:.2f}, setup/other {setup1:.2f})")
     for ngpu in (2, 4, 8):
+        # filter alone: the widest shard's padded DMMA work sets the time
+        tf1 = sum(i[2] for i in its)
+        tfn = sum(DEGREE * interp(step, -(-i[0] // ngpu)) for i in its if i[0])
+        print(f"N={ngpu}: filter-only bound {tf1 / (ngpu * tfn):.3f} "
+              f"(1-GPU filter {tf1:.1f} s, per-rank filter {tfn:.1f} s)")
         new = old = 0.0
         for cols, _, tf, tq, tr in its:
             kp = -(-cols // ngpu)
