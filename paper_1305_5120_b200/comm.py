@@ -22,6 +22,7 @@ and stream, and returns every rank's result (re-raising the first failure).
 
 import copy
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -221,7 +222,7 @@ def set_devices(devices):
 def get_devices():
     if _default_devices is not None:
         return list(_default_devices)
-    env = __import__("os").environ.get("CHFSI_DEVICES", "").strip()
+    env = os.environ.get("CHFSI_DEVICES", "").strip()
     if not env:
         return None
     return normalize_devices(int(env) if env.isdigit() else [int(x) for x in env.split(",")])
