@@ -501,7 +501,7 @@ def test_filter_width_rule_large_operator(eng):
     H = H.contiguous()
     eng.declare_operator(H)
     try:
-        for k in (1, 8, 26, 40, 100, 550):
+        for k in (1, 8, 26, 40, 51, 100, 101, 201, 550):
             cfg, split = ctypes.c_int(), ctypes.c_int()
             _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg),
                          ctypes.byref(split))
