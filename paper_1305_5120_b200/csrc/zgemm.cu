@@ -318,10 +318,33 @@ long long rule_min_m() {
 }
 constexpr double kRuleTargetCtas = 20000.0;
 
+// Power: a sum-plane kernel streams H and its 3M sum plane (24 bytes per element of
+// H); on a block of one 32-column tile that is 9.6 GB per step at n = 20000, and the
+// B200 then runs at its 1 kW cap with the SM clock at ~1700 MHz (sustained degree-25
+// filter calls, profiles/r02/narrow_plans.json: k = 26 2.50 ms per step at 995 W). The
+// in-loop-sum 3M kernel reads H alone (16 bytes per element), stays at 1965 MHz and
+// takes 2.34 ms (k = 32: 2.54 -> 2.36 ms). From two column tiles up the sum planes win
+// again (k = 40: 3.41 vs 4.13 ms; k = 64: equal; k >= 80 sum planes ahead), and at
+// k <= 16 the sum-plane kernel, HBM-bound, is ahead too. CHFSI_NARROW_INLOOP=0 disables.
+bool narrow_inloop(long long N) {
+  static const bool on = [] {
+    const char* e = getenv("CHFSI_NARROW_INLOOP");
+    return !(e && atoi(e) == 0);
+  }();
+  return on && N > 16 && N <= 32;
+}
+
 Plan choose_sums_rule(long long M, long long N, long long K) {
   Plan best;
   double best_score = 1e300;
   const long long tm = (M + 63) / 64;
+  if (narrow_inloop(N)) {
+    const long long ktiles = std::max<long long>(1, (K + 7) / 8);
+    best.cfg = FIRST_3M;  // cfg 11: 64x32, 3M with the operand sums formed in the loop
+    best.split = (int)std::min<long long>(8, std::max<long long>(1, ktiles / 4));
+    best.k_chunk = (int)(((ktiles + best.split - 1) / best.split) * 8);
+    return best;
+  }
   for (int c = FIRST_SUMS; c < NCFG; ++c) {
     const long long tn = (N + kBN[c] - 1) / kBN[c];
     const long long last = (N - (tn - 1) * kBN[c] + 7) / 8;

@@ -505,7 +505,12 @@ def test_filter_width_rule_large_operator(eng):
             cfg, split = ctypes.c_int(), ctypes.c_int()
             _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg),
                          ctypes.byref(split))
-            assert cfg.value >= _SUMS_FIRST, (k, cfg.value)
+            # one 32-column tile (17-32 columns): the in-loop-sum 3M kernel (cfg 11),
+            # which does not stream H's sum plane (the power-capped regime, zgemm.cu)
+            if 16 < k <= 32:
+                assert cfg.value == 11, (k, cfg.value)
+            else:
+                assert cfg.value >= _SUMS_FIRST, (k, cfg.value)
             Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
             W = torch.empty_like(Y)
             a, b, lam_ref = -1.0, 1.0, -2.0
