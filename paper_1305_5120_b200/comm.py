@@ -117,6 +117,7 @@ class _Clique:
         self.barrier = threading.Barrier(self.world)
         self.slots = [None] * self.world
         self.handles = []
+        self.broken = False
         if backend == "nccl":
             from . import _native
             lib = _native.load()
@@ -126,6 +127,7 @@ class _Clique:
             self.handles = [ctypes.c_void_p(h) for h in hs]
 
     def abort(self):
+        self.broken = True
         self.barrier.abort()
         if self.handles:
             from . import _native
@@ -270,7 +272,6 @@ def run_on_devices(devices, fn, backend=None):
     CUDA device set, with its own stream and engine handle) and return the results in
     rank order. The first exception is re-raised after every thread has ended; a
     failing rank aborts the clique so the others do not wait forever."""
-    from . import device as dev
     devices = normalize_devices(devices)
     if backend is None:
         backend = choose_backend(devices)
@@ -280,7 +281,33 @@ def run_on_devices(devices, fn, backend=None):
     # completes before any rank thread runs on its own stream
     for d in sorted(set(devices)):
         torch.cuda.synchronize(d)
-    clique = _Clique(devices, backend)
+    with _clique_lock:  # one in-process group at a time owns a clique
+        return _run(devices, backend, fn)
+
+
+# NCCL cliques are kept for the next call on the same devices (ncclCommInitAll costs
+# far more than a small solve); release_devices() destroys them.
+_cliques = {}
+_clique_lock = threading.RLock()
+
+
+def release_devices():
+    """Destroy the cached in-process NCCL cliques."""
+    with _clique_lock:
+        for c in _cliques.values():
+            c.close()
+        _cliques.clear()
+
+
+def _run(devices, backend, fn):
+    from . import device as dev
+    key = (tuple(devices), backend)
+    clique = _cliques.get(key)
+    if clique is None or clique.broken:
+        if clique is not None:
+            clique.close()
+        clique = _Clique(devices, backend)
+        _cliques[key] = clique
     results = [None] * clique.world
     errors = [None] * clique.world
 
@@ -304,7 +331,10 @@ def run_on_devices(devices, fn, backend=None):
         t.start()
     for t in threads:
         t.join()
-    clique.close()
+    clique.slots = [None] * clique.world  # drop the last call's tensors
+    if clique.broken:  # an aborted clique is not reused
+        clique.close()
+        _cliques.pop(key, None)
     # the root cause, not a secondary "group aborted" of a waiting rank
     first = next((e for e in errors if e is not None and not _is_abort(e)), None)
     if first is None:

@@ -436,3 +436,29 @@ def test_bench_nccl_refuses_more_gpus_than_visible():
         [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--no-extras"],
         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode != 0 and "visible GPUs" in out.stderr
+
+
+@pytest.mark.gpu
+def test_in_process_clique_is_reused_and_replaced_after_abort():
+    """run_on_devices keeps the clique of a device set for the next call (NCCL
+    communicator setup costs more than a small solve); a clique aborted by a failing
+    rank is dropped and the next call gets a fresh one."""
+    from paper_1305_5120_b200 import comm
+    comm.release_devices()
+    out1 = comm.run_on_devices([0, 0], lambda c: c.rank)
+    c1 = comm._cliques[((0, 0), "local")]
+    out2 = comm.run_on_devices([0, 0], lambda c: c.world)
+    assert out1 == [0, 1] and out2 == [2, 2]
+    assert comm._cliques[((0, 0), "local")] is c1 and not c1.broken
+
+    def fail(c):
+        if c.rank == 1:
+            raise RuntimeError("rank 1 fails")
+        c.barrier()  # rank 0 waits for rank 1: must be released by the abort
+
+    with pytest.raises(RuntimeError, match="rank 1 fails"):
+        comm.run_on_devices([0, 0], fail)
+    assert ((0, 0), "local") not in comm._cliques and c1.broken
+    assert comm.run_on_devices([0, 0], lambda c: c.rank) == [0, 1]
+    comm.release_devices()
+    assert not comm._cliques
