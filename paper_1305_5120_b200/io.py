@@ -17,7 +17,7 @@ import numpy as np
 from .errors import BadMagic, ContractViolation, MatrixFileError, SymmetryViolation, TruncatedPayload
 
 __all__ = ["MAGIC", "write_matrix", "read_matrix", "read_header", "read_payload",
-           "normalize_phase"]
+           "normalize_phase", "save_sequence", "load_sequence"]
 
 MAGIC = b"CHFSI-MAT1"
 KIND_BYTES = {"hermitian": b"H", "spd": b"S", "block": b"B"}
@@ -137,3 +137,84 @@ def normalize_phase(block):
             arr2[:, j] *= np.conj(pivot) / mag
             arr2[i, j] = mag  # exactly real
     return arr2 if arr.ndim == 2 else arr2[:, 0]
+
+
+# ----------------------------------------------------------------------
+# sequence manifests (reference io.py:300-368): one CHFSI-MAT1 file per cycle matrix
+# plus a text manifest with the SequenceSpec fields and the cycle -> file map; the same
+# file names and manifest text as the reference, so either side reads the other's.
+
+_SPEC_TYPES = {"n": int, "N": int, "nev": int, "delta0": float, "rho": float, "seed": int,
+               "kind": str, "vary_b": bool, "band_max": float, "gap": float, "spread": float}
+
+
+def save_sequence(seq, directory, stem="cycle"):
+    """Write every cycle of a ProblemSequence (<stem>_0001_A.mat, + _B.mat for generalized
+    problems) and <stem>_manifest.txt; returns the manifest path. A matrix shared by
+    consecutive cycles (a fixed B) is written once per cycle, as by the reference."""
+    from dataclasses import fields
+    os.makedirs(directory, exist_ok=True)
+    spec = seq.spec
+    lines = ["# chfsi sequence manifest"]
+    for f in fields(spec):
+        lines.append(f"{f.name} = {getattr(spec, f.name)}")
+    for ell, (a_mat, b_mat) in enumerate(seq.problems, start=1):
+        a_name = f"{stem}_{ell:04d}_A.mat"
+        write_matrix(os.path.join(directory, a_name), a_mat, kind="hermitian")
+        if b_mat is None:
+            lines.append(f"cycle {ell}: {a_name}")
+        else:
+            b_name = f"{stem}_{ell:04d}_B.mat"
+            write_matrix(os.path.join(directory, b_name), b_mat, kind="spd")
+            lines.append(f"cycle {ell}: {a_name} {b_name}")
+    manifest = os.path.join(directory, f"{stem}_manifest.txt")
+    with open(manifest, "w", encoding="utf-8") as fh:
+        fh.write("\n".join(lines) + "\n")
+    return manifest
+
+
+def load_sequence(manifest_path, device=None):
+    """Rebuild a ProblemSequence from a manifest: every matrix goes straight from its file
+    into pinned memory and HBM (read_matrix); B files with identical bytes (a fixed
+    metric) become ONE device matrix, so its Cholesky factor is computed once for the
+    whole sequence (solve_generalized caches it on the object)."""
+    import hashlib
+
+    from .errors import ConfigError
+    from .sequence import ProblemSequence, SequenceSpec
+    base = os.path.dirname(os.path.abspath(manifest_path))
+    spec_vals, cycles = {}, []
+    with open(manifest_path, "r", encoding="utf-8") as fh:
+        for line in fh:
+            body = line.split("#", 1)[0].strip()
+            if not body:
+                continue
+            if body.startswith("cycle "):
+                idx, names = body[len("cycle "):].split(":", 1)
+                cycles.append((int(idx), names.split()))
+            elif "=" in body:
+                key, raw = (t.strip() for t in body.split("=", 1))
+                if key not in _SPEC_TYPES:
+                    raise ConfigError(f"manifest: unknown spec key {key!r}")
+                typ = _SPEC_TYPES[key]
+                spec_vals[key] = raw.lower() in ("true", "yes", "1") if typ is bool else typ(raw)
+    spec = SequenceSpec(**spec_vals)
+    cycles.sort()
+    problems, shared = [], {}
+    for _, names in cycles:
+        a_mat = read_matrix(os.path.join(base, names[0]), device=device)
+        b_mat = None
+        if len(names) > 1:
+            path = os.path.join(base, names[1])
+            h = hashlib.sha256()
+            with open(path, "rb") as fb:
+                for chunk in iter(lambda: fb.read(1 << 24), b""):
+                    h.update(chunk)
+            key = h.hexdigest()
+            if key not in shared:
+                shared[key] = read_matrix(path, device=device)
+            b_mat = shared[key]
+        problems.append((a_mat, b_mat))
+    if len(problems) != spec.N:
+        raise ConfigError(f"manifest lists {len(problems)} cycles but spec says N = {spec.N}")
+    return ProblemSequence(spec=spec, problems=problems)

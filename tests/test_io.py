@@ -84,3 +84,50 @@ def test_read_matrix_onto_device(tmp_path):
     cio.write_matrix(p, skew)
     with pytest.raises(SymmetryViolation):
         cio.read_matrix(p)
+
+
+def _manifest_dir():
+    return os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "manifest")
+
+
+def test_save_sequence_byte_identical_to_reference(tmp_path):
+    """save_sequence writes the same per-cycle CHFSI-MAT1 files and manifest text as the
+    reference's save_sequence (io.py:300-333; tests/golden/manifest was written by it)."""
+    from paper_1305_5120_b200.io import read_payload, save_sequence
+    from paper_1305_5120_b200.sequence import ProblemSequence, SequenceSpec
+    ref = _manifest_dir()
+    probs = []
+    for ell in range(1, 4):
+        a = read_payload(os.path.join(ref, f"gen_{ell:04d}_A.mat"))[1]
+        b = read_payload(os.path.join(ref, f"gen_{ell:04d}_B.mat"))[1]
+        probs.append((a, b))
+    seq = ProblemSequence(spec=SequenceSpec(n=12, N=3, nev=3, seed=4, kind="generalized"),
+                          problems=probs)
+    manifest = save_sequence(seq, str(tmp_path), stem="gen")
+    assert os.path.basename(manifest) == "gen_manifest.txt"
+    for name in sorted(os.listdir(ref)):
+        with open(os.path.join(ref, name), "rb") as f1, open(tmp_path / name, "rb") as f2:
+            assert f1.read() == f2.read(), name
+
+
+def test_manifest_parse_errors(tmp_path):
+    from paper_1305_5120_b200.errors import ConfigError
+    from paper_1305_5120_b200.io import load_sequence
+    bad = tmp_path / "m.txt"
+    bad.write_text("# chfsi sequence manifest\nn = 12\nbogus = 3\n")
+    with pytest.raises(ConfigError, match="unknown spec key"):
+        load_sequence(str(bad))
+
+
+@pytest.mark.gpu
+def test_load_sequence_reference_manifest_to_device():
+    """load_sequence reads the reference's manifest onto the GPU; the fixed metric B of a
+    generalized sequence becomes one device matrix shared by every cycle."""
+    from paper_1305_5120_b200.io import load_sequence, read_payload
+    seq = load_sequence(os.path.join(_manifest_dir(), "gen_manifest.txt"))
+    assert seq.spec.kind == "generalized" and seq.spec.N == 3 and len(seq.problems) == 3
+    bs = [b for _, b in seq.problems]
+    assert bs[0] is bs[1] is bs[2]
+    for ell, (a, b) in enumerate(seq.problems, start=1):
+        ra = read_payload(os.path.join(_manifest_dir(), f"gen_{ell:04d}_A.mat"))[1]
+        assert np.max(np.abs(a.entries - (ra + ra.conj().T) / 2)) <= 1e-15 * np.max(np.abs(ra))
