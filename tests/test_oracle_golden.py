@@ -134,3 +134,24 @@ def test_sequence_reuse_fixture():
         assert close(lam, g[f"lam{i}"], 1e-12)
         assert rep["total_matmuls"] == int(g[f"work{i}"])
         assert len(rep["iterations"]) == int(g[f"iters{i}"])
+
+
+def test_c1_full_fixture_trace_prefix():
+    """BASELINE config 1, problem 1 (n = 2000, nev = 200, nex = 40, m = 20; the reference's
+    own solve_sequence run, tests/golden/c1_full.npz): the oracle, seeded like the
+    reference's sequence driver (solver Generator [0, 11, 1]), retraces the first 25
+    outer iterations -- converged counts and residual extremes."""
+    import os
+    path = os.path.join(GOLD, "c1_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("c1_full.npz not generated")
+    g = np.load(path)
+    a, _ = baseline_sequence(0, 2000, 1)[0]
+    with pytest.raises(O.OracleError) as exc:
+        O.solve(a, None, 200, 40, 20, 1e-10, 25, seed=np.random.default_rng([0, 11, 1]))
+    rep = exc.value.info["report"]
+    conv = [r["converged"] for r in rep["iterations"]]
+    assert conv == g["it_converged0"][:25].tolist()
+    assert [r["filtered_cols"] for r in rep["iterations"]] == g["it_filtered0"][:25].tolist()
+    mr = np.array([r["max_resid"] for r in rep["iterations"]])
+    assert np.max(np.abs(mr - g["it_max_resid0"][:25]) / g["it_max_resid0"][:25]) <= 1e-6
