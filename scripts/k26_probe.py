@@ -1,3 +1,7 @@
+"""Filter step time at narrow widths (k = 26, 51, 101, 201; n = 20000) for degree-5 and
+degree-25 calls, start blocks of scale 1 and 7e-6, on the c4 matrix and on a random
+Hermitian one: the sustained narrow-width slowdown traced to the board power cap
+(profiles/r02/narrow_plans.json). python scripts/k26_probe.py"""
 import sys, math, json, torch, numpy as np
 sys.path.insert(0, ".")
 from paper_1305_5120_b200 import device as D

@@ -17,7 +17,7 @@ from paper_1305_5120_b200 import _native, device as D  # noqa: E402
 from paper_1305_5120_b200 import workloads as Wl  # noqa: E402
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 26
-n = 20000
+n = int(os.environ.get("N_ORDER", "20000"))
 dev = torch.device("cuda", 0)
 eng = D.Engine.get(dev)
 lib = _native.load()
@@ -25,7 +25,7 @@ H, lam = Wl.spectrum_matrix_torch(0, n, dev)
 g = torch.Generator(device=dev)
 g.manual_seed(1)
 eng.declare_operator(H)
-a, b, lr = float(lam[2000]), 1.01 * float(lam[-1]), float(lam[0])
+a, b, lr = float(lam[n // 10]), 1.01 * float(lam[-1]), float(lam[0])
 Y0 = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
 Y, W = Y0.clone(), torch.empty_like(Y0)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

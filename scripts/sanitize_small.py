@@ -58,7 +58,31 @@ eng.declare_operator(None)
 Hbig = torch.randn((8192, 8192), dtype=torch.complex128, device=eng.device)
 eng.filter(Hbig, torch.randn((26, 8192), dtype=torch.complex128, device=eng.device),
            torch.empty((26, 8192), dtype=torch.complex128, device=eng.device), 2, -1.0, 1.0, -2.0)
+# round 2: the narrow rule's in-loop kernel (17-32 columns) and a two-tile block
+for kk in (20, 40):
+    eng.filter(Hbig, torch.randn((kk, 8192), dtype=torch.complex128, device=eng.device),
+               torch.empty((kk, 8192), dtype=torch.complex128, device=eng.device), 2, -1.0, 1.0,
+               -2.0)
 del Hbig
+# round 2: the HBM-bound GEMV (N = 1) with a padded leading dimension, and the Lanczos bound
+Abuf = torch.randn((300, 310), dtype=torch.complex128, device=eng.device)
+x = torch.randn((1, 300), dtype=torch.complex128, device=eng.device)
+y = torch.randn((1, 300), dtype=torch.complex128, device=eng.device)
+eng.zgemm("N", "N", 300, 1, 300, 0.5 + 0.1j, Abuf[:, :300], x, -0.2, y)
+hl = (Abuf[:, :300] + Abuf[:, :300].T.conj()).resolve_conj().contiguous()
+eng.lanczos_bound(hl, x[0], 10)
+# round 2: triangular operand at an unaligned offset with a forced split (element-masked)
+lib.chfsi_gemm_override(-1, 3)
+L = torch.tril(torch.randn((64, 64), dtype=torch.complex128, device=eng.device)).T.contiguous()
+eng.zgemm("N", "N", 20, 17, 64, 1.0, torch.randn((64, 20), dtype=torch.complex128,
+                                                  device=eng.device),
+          L[3:20], 0.0, torch.empty((17, 20), dtype=torch.complex128, device=eng.device),
+          tri=eng.TRI_B_LOWER, tri_offset=3)
+lib.chfsi_gemm_override(-1, 0)
+# round 2: pageable upload through the staging ring (> 8 MB, several chunks)
+big = np.asfortranarray(crand(3000, 400))
+t = D.to_device(big, eng.device)
+assert np.array_equal(D.to_host(t), big)
 from paper_1305_5120_b200.workloads import baseline_matrix  # noqa: E402
 h, lam, _ = baseline_matrix(1, 120)
 lam_g, v, rep = G.chfsi_solve(h, None, G.SolverConfig(nev=10, buffer=6, degree=12,
