@@ -61,6 +61,10 @@ def parse():
     ap.add_argument("--legs", default="",
                     help="comma list: run only these extra legs (development; default all)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--time-budget-s", type=float, default=840.0,
+                    help="an optional leg is skipped (and says so in the line) when the "
+                         "process has already run this long minus the leg's usual duration, "
+                         "so the JSON line is printed before any outer limit")
     ap.add_argument("--complex-mul", type=int, default=3, choices=[3, 4],
                     help="complex products of the GEMMs: 3 (3M, default) or 4 real DMMA "
                          "products (the north star's literal four-MMA form)")
@@ -69,9 +73,24 @@ def parse():
     return ap.parse_args()
 
 
+T_PROCESS_START = time.monotonic()
+
+# usual duration of the long optional legs on one B200 (s), for the time budget
+LEG_SECONDS = {"solve_c4": 100.0, "solve_c4_reference_window": 45.0, "sequence_c4": 190.0,
+               "solve_c0": 30.0, "sequence_c1": 30.0, "generalized_c4_setup": 15.0,
+               "e2e_pageable": 20.0, "tail": 10.0, "filter_complex_mul_4": 20.0,
+               "filter_complex_mul_3": 20.0}
+
+
 def want(args, key):
     """Extra legs to run: all by default, or the --legs subset."""
     return not args.legs or key in args.legs.split(",")
+
+
+def in_budget(args, key):
+    """False when starting this optional leg now would run past --time-budget-s."""
+    elapsed = time.monotonic() - T_PROCESS_START
+    return elapsed + LEG_SECONDS.get(key, 0.0) <= args.time_budget_s
 
 
 def workload_cfg(args, n_gpus):
@@ -358,15 +377,22 @@ def run_b200(args, rank, world, local_rank):
         if not args.no_extras:
             # s per ChFSI solve at the metric's n on all ranks (column-sharded)
             nev_s = int(round(k * 2000 / 2200))
-            if want(args, "solve_c4"):
-                solve = guarded_leg(line, rank, lambda: solve_c4_leg(H, lam, rank, world, dev,
-                                                                     nev_s, k - nev_s, m))
-                if rank == 0:
-                    line["solve_c4"] = solve
-            for key, fn in extra_solve_legs(H, lam, rank, world, dev, nev_s, k - nev_s, m):
+            def agreed_in_budget(key):
+                # rank 0 decides for everyone (the legs have collectives inside)
+                flag = torch.tensor([1 if in_budget(args, key) else 0], device=dev)
+                dist.broadcast(flag, 0)
+                return bool(flag.item())
+
+            legs = [("solve_c4", lambda: solve_c4_leg(H, lam, rank, world, dev, nev_s,
+                                                      k - nev_s, m))]
+            legs += extra_solve_legs(H, lam, rank, world, dev, nev_s, k - nev_s, m)
+            for key, fn in legs:
                 if not want(args, key):
                     continue
-                out = guarded_leg(line, rank, fn, key=key)
+                if not agreed_in_budget(key):
+                    out = {"skipped": f"time budget ({args.time_budget_s:.0f} s)"}
+                else:
+                    out = guarded_leg(line, rank, fn, key=key)
                 if rank == 0:
                     line[key] = out
         if rank == 0:
@@ -412,43 +438,52 @@ def finish_single_gpu(args, line, eng, H, Yfull, Y0, Y, W, lam, a_edge, b_up, la
             # an optional leg must never cost the headline line
             if not want(args, key):
                 return
+            if not in_budget(args, key):
+                line[key] = {"skipped": f"time budget ({args.time_budget_s:.0f} s)"}
+                return
             try:
                 line[key] = fn()
             except Exception as exc:  # pragma: no cover - reported, not raised
                 line[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
             torch.cuda.empty_cache()
 
+        # the contract's keys first (e2e, cpu_baseline), then the optional legs in the
+        # order of what they explain; a leg that would run past --time-budget-s is skipped
         leg("e2e", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev))
-        leg("e2e_pageable", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev,
-                                            pinned=False))
-        leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
-        other = 4 if args.complex_mul == 3 else 3
-        leg(f"filter_complex_mul_{other}",
-            lambda: filter_other_mul(eng, H, Y0, Y, W, m, a_edge, b_up, lam_ref, other))
         # host copies for the CPU baseline leg (the same H and full block)
         h_host = H.cpu().numpy().T
         y_host = Yfull.cpu().numpy().T
-        del Yfull, Y0, Y, W
-        torch.cuda.empty_cache()
-        nev_s = int(round(args.k * 2000 / 2200))
-        if want(args, "solve_c4"):
-            line["solve_c4"] = guarded_leg(line, 0, lambda: solve_c4_leg(
-                H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree))
-        for key, fn in extra_solve_legs(H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree):
-            if want(args, key):
-                line[key] = guarded_leg(line, 0, fn, key=key)
-                torch.cuda.empty_cache()
-        del H
-        torch.cuda.empty_cache()
-        leg("solve_c0", solve_c0)
-        leg("sequence_c1", sequence_c1)
-        leg("generalized_c4_setup", generalized_c4_setup)
 
         def cpu_leg():
             rate, sample, cores = cpu_filter_rate(h_host, y_host, lam, args.cpu_seconds)
             return {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
         leg("cpu_baseline", cpu_leg)
         del h_host, y_host
+        leg("e2e_pageable", lambda: e2e_leg(args, H, Yfull, a_edge, b_up, lam_ref, dev,
+                                            pinned=False))
+        leg("tail", lambda: tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref))
+        other = 4 if args.complex_mul == 3 else 3
+        leg(f"filter_complex_mul_{other}",
+            lambda: filter_other_mul(eng, H, Y0, Y, W, m, a_edge, b_up, lam_ref, other))
+        del Yfull, Y0, Y, W
+        torch.cuda.empty_cache()
+        nev_s = int(round(args.k * 2000 / 2200))
+        legs = [("solve_c4", lambda: solve_c4_leg(H, lam, 0, 1, dev, nev_s, args.k - nev_s,
+                                                  args.degree))]
+        legs += extra_solve_legs(H, lam, 0, 1, dev, nev_s, args.k - nev_s, args.degree)
+        for key, fn in legs:
+            if not want(args, key):
+                continue
+            if not in_budget(args, key):
+                line[key] = {"skipped": f"time budget ({args.time_budget_s:.0f} s)"}
+                continue
+            line[key] = guarded_leg(line, 0, fn, key=key)
+            torch.cuda.empty_cache()
+        del H
+        torch.cuda.empty_cache()
+        leg("solve_c0", solve_c0)
+        leg("sequence_c1", sequence_c1)
+        leg("generalized_c4_setup", generalized_c4_setup)
     print(json.dumps(line), flush=True)
 
 

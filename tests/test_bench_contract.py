@@ -53,3 +53,19 @@ def test_guarded_leg_reports_errors_and_abandons_a_stuck_leg():
     assert len(lines) == 1 and "not reached" not in res.stdout
     d = json.loads(lines[0])
     assert d["value"] == 2.0 and "abandoned" in d["solve_c4"]["error"]
+
+
+def test_time_budget_skips_a_leg_that_would_overrun():
+    """bench.in_budget: an optional leg starts only when its usual duration still fits in
+    --time-budget-s of process time, so the JSON line is printed before an outer limit."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+
+    elapsed = bench.time.monotonic() - bench.T_PROCESS_START
+    roomy = argparse.Namespace(time_budget_s=elapsed + 10_000.0)
+    tight = argparse.Namespace(time_budget_s=elapsed + 60.0)
+    assert bench.in_budget(roomy, "sequence_c4")
+    assert not bench.in_budget(tight, "sequence_c4")      # ~190 s does not fit in 60 s
+    assert bench.in_budget(tight, "tail")                  # ~10 s does
+    assert bench.in_budget(tight, "e2e") and bench.in_budget(tight, "cpu_baseline")
