@@ -505,6 +505,8 @@ KERNELS = {
     14: "zgemm_tma_kernel<64,32,warp32x16,TMA+mbarrier x4,EPI_FILTER,3M,sum planes>",
     15: "zgemm_tma_kernel<64,32,warp16x32,TMA+mbarrier x4,EPI_FILTER,3M,sum planes>",
     16: "zgemm_tma_kernel<64,24,warp16x24,TMA+mbarrier x4,EPI_FILTER,3M,sum planes>",
+    17: "zgemm_tma_kernel<64,32,warp16x32,TMA+mbarrier x4,EPI_FILTER,3M,B-sum plane>",
+    18: "zgemm_tma_kernel<64,24,warp16x24,TMA+mbarrier x4,EPI_FILTER,3M,B-sum plane>",
 }
 
 

@@ -88,10 +88,11 @@ struct CfgT {
   static KFn fn() { return &zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, OPA, OPB, EPI>; }
 };
 
-constexpr int NCFG = 17;
+constexpr int NCFG = 19;
 constexpr int FIRST_TMA = 7;  // cfgs >= 7: TMA + mbarrier kernels (zgemm_tma.cuh), op N x N only
 constexpr int FIRST_3M = 11;  // cfgs >= 11: the TMA kernels with 3M complex products
 constexpr int FIRST_SUMS = 14;  // cfgs >= 14: 3M reading precomputed operand-sum planes
+constexpr int FIRST_BSUMS = 17; // cfgs >= 17: 3M reading the B-sum plane only (A sums in the loop)
 // cfg 0: 64x64   BK8  warp 32x32 (4 warps)     cfg 4: 64x64  BK16 warp 32x32, 3 stages
 // cfg 1: 64x32   BK8  warp 32x16 (4 warps)     cfg 5: 128x64 BK8  warp 32x32 (8 warps)
 // cfg 2: 64x16   BK8  warp 16x16 (4 warps)     cfg 6: 128x32 BK8  warp 32x16 (8 warps)
@@ -108,7 +109,7 @@ using C6 = CfgT<128, 32, 8, 32, 16, 4>;
 // cfg 7; on a ragged column edge every warp keeps the same number of live 8-column blocks)
 using TmaFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
                       const CUtensorMap, const GemmParams);
-template <int BM, int BN, int WM, int WN, int ST, int MINB = 1, int MUL = 4, bool SUMS = false>
+template <int BM, int BN, int WM, int WN, int ST, int MINB = 1, int MUL = 4, int SUMS = SUMS_NONE>
 struct TmaT {
   static constexpr int threads = (BM / WM) * (BN / WN) * 32;
   static constexpr int smem() { return zgemm_tma_smem_bytes<BM, BN, WM, WN, ST, SUMS>(); }
@@ -129,16 +130,21 @@ using T12 = TmaT<64, 32, 16, 32, 4, 3, 3>;
 // cfg 13: 3M, 64x32 with eight 16x16 warps (24 accumulator doubles: 2 CTAs / SM = 16 warps)
 using T13 = TmaT<64, 32, 16, 16, 4, 2, 3>;
 // cfg 14 / 15: cfg 11 / 12 reading precomputed operand-sum planes (3M without in-loop DADDs)
-using T14 = TmaT<64, 32, 32, 16, 4, 3, 3, true>;
-using T15 = TmaT<64, 32, 16, 32, 4, 3, 3, true>;
+using T14 = TmaT<64, 32, 32, 16, 4, 3, 3, SUMS_BOTH>;
+using T15 = TmaT<64, 32, 16, 32, 4, 3, 3, SUMS_BOTH>;
 // cfg 16: sum planes, 64x24 tile of four 16x24 warps stacked by rows: 24-column tiles
 // fit block widths that 32-column tiles round up badly (a 550-column shard: 23 x 24 =
 // 552 vs 18 x 32 = 576 columns of work)
-using T16 = TmaT<64, 24, 16, 24, 4, 3, 3, true>;
-const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64, 64, 64, 64};
-const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32, 32, 32, 24};
-const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8};
-const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16, 16, 32, 24};  // warp tile width
+using T16 = TmaT<64, 24, 16, 24, 4, 3, 3, SUMS_BOTH>;
+// cfg 17 / 18: cfg 15 / 16 reading only the B-sum plane: H streams at 16 bytes per element
+// (no H sum plane) and Ar + Ai costs FM = 2 DADDs per 24 (18) DMMAs -- the narrow-block
+// plan, where streaming 24 bytes per element of H holds the board at its power cap
+using T17 = TmaT<64, 32, 16, 32, 4, 3, 3, SUMS_B>;
+using T18 = TmaT<64, 24, 16, 24, 4, 3, 3, SUMS_B>;
+const int kBM[NCFG] = {64, 64, 64, 32, 64, 128, 128, 64, 64, 64, 64, 64, 64, 64, 64, 64, 64, 64, 64};
+const int kBN[NCFG] = {64, 32, 16, 16, 64, 64, 32, 32, 16, 64, 32, 32, 32, 32, 32, 32, 24, 32, 24};
+const int kBKc[NCFG] = {8, 8, 8, 8, 16, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8, 8};
+const int kWN[NCFG] = {32, 16, 16, 8, 32, 32, 16, 16, 16, 32, 32, 16, 32, 16, 16, 32, 24, 32, 24};  // warp tile width
 bool g_tma_enabled = true;
 // complex products in the TMA kernels: 3 (3M, default) or 4 real DMMA products
 int g_mul = [] {
@@ -243,6 +249,8 @@ void fill_table() {
   put_tma<T14>(14);
   put_tma<T15>(15);
   put_tma<T16>(16);
+  put_tma<T17>(17);
+  put_tma<T18>(18);
 }
 
 struct Plan {
@@ -263,7 +271,8 @@ struct Plan {
 //     warps (ncu: DMMA pipe 92.5 % vs 95.7 % active at k = 210): x (1 + kRag / tiles_n);
 //   * split-K adds the reduce pass: kTred + (s + 3) M N 16 B at HBM speed.
 constexpr double kEffNN[NCFG] = {0.906, 0.898, 0.837, 0.823, 0.911, 0.926, 0.885,
-                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13, 1.27, 1.26, 1.24};
+                                 0.966, 0.915, 0.962, 0.954, 1.17, 1.16, 1.13, 1.27, 1.26, 1.24,
+                                 1.22, 1.20};
 constexpr double kEffCN[7] = {0.886, 0.927, 0.877, 0.854, 1.058, 0.971, 0.887};
 constexpr double kR0Warps4 = 1.289, kR0Warps8 = 1.108;
 constexpr double kRag = 0.122, kFloor = 0.859;
@@ -319,33 +328,43 @@ long long rule_min_m() {
 constexpr double kRuleTargetCtas = 20000.0;
 
 // Power: a sum-plane kernel streams H and its 3M sum plane (24 bytes per element of
-// H); on a block of one 32-column tile that is 9.6 GB per step at n = 20000, and the
-// B200 then runs at its 1 kW cap with the SM clock at ~1700 MHz (sustained degree-25
-// filter calls, profiles/r02/narrow_plans.json: k = 26 2.50 ms per step at 995 W). The
-// in-loop-sum 3M kernel reads H alone (16 bytes per element), stays at 1965 MHz and
-// takes 2.34 ms (k = 32: 2.54 -> 2.36 ms). From two column tiles up the sum planes win
-// again (k = 40: 3.41 vs 4.13 ms; k = 64: equal; k >= 80 sum planes ahead), and at
-// k <= 16 the sum-plane kernel, HBM-bound, is ahead too. CHFSI_NARROW_INLOOP=0 disables.
+// H); on a narrow block that is 9.6 GB per step at n = 20000 for little tensor work, and
+// the B200 then runs at its 1 kW cap with the SM clock well under 1965 MHz (sustained
+// degree-25 filter calls, profiles/r02/narrow_plans.json: k = 26 2.50 ms per step at
+// 1700 MHz, k = 51 4.27 ms at 1777 MHz, k = 101 7.98 ms at 1867 MHz). The B-sum-only
+// kernels (cfg 17 / 18) read H alone (16 bytes per element) and form Ar + Ai in the loop
+// (2 DADDs per 24 DMMAs; the all-in-loop kernel cfg 11 / 12 pays 6). Blocks of
+// bsums_min_n() .. bsums_max_n() columns take them; CHFSI_NARROW_INLOOP=0 disables.
+long long bsums_min_n() {
+  static const long long v = [] {
+    const char* e = getenv("CHFSI_BSUMS_MIN_N");  // tuning only
+    return e ? atoll(e) : 17LL;
+  }();
+  return v;
+}
+long long bsums_max_n() {
+  static const long long v = [] {
+    const char* e = getenv("CHFSI_BSUMS_MAX_N");  // tuning only
+    return e ? atoll(e) : 64LL;
+  }();
+  return v;
+}
 bool narrow_inloop(long long N) {
   static const bool on = [] {
     const char* e = getenv("CHFSI_NARROW_INLOOP");
     return !(e && atoi(e) == 0);
   }();
-  return on && N > 16 && N <= 32;
+  return on && N >= bsums_min_n() && N <= bsums_max_n();
 }
 
 Plan choose_sums_rule(long long M, long long N, long long K) {
   Plan best;
   double best_score = 1e300;
   const long long tm = (M + 63) / 64;
-  if (narrow_inloop(N)) {
-    const long long ktiles = std::max<long long>(1, (K + 7) / 8);
-    best.cfg = FIRST_3M;  // cfg 11: 64x32, 3M with the operand sums formed in the loop
-    best.split = (int)std::min<long long>(8, std::max<long long>(1, ktiles / 4));
-    best.k_chunk = (int)(((ktiles + best.split - 1) / best.split) * 8);
-    return best;
-  }
-  for (int c = FIRST_SUMS; c < NCFG; ++c) {
+  // the kernel family: both sum planes, or (narrow blocks) the B-sum plane only
+  const bool bonly = narrow_inloop(N);
+  const int c_lo = bonly ? FIRST_BSUMS : FIRST_SUMS, c_hi = bonly ? NCFG : FIRST_BSUMS;
+  for (int c = c_lo; c < c_hi; ++c) {
     const long long tn = (N + kBN[c] - 1) / kBN[c];
     const long long last = (N - (tn - 1) * kBN[c] + 7) / 8;
     const int per = kWN[c] / 8, wcols = kBN[c] / kWN[c];
@@ -374,6 +393,7 @@ Plan choose_sums_rule(long long M, long long N, long long K) {
   int s_best = 1;
   for (int s : kSplits)
     if (std::fabs(std::log((double)s / s_t)) < std::fabs(std::log((double)s_best / s_t))) s_best = s;
+  if (bonly && tn == 1) s_best = std::min(s_best, 8);  // one column tile: split 8 measured best
   best.split = (int)std::max<long long>(1, std::min<long long>(s_best, s_max));
   best.k_chunk = (int)(((ktiles + best.split - 1) / best.split) * 8);
   return best;
@@ -397,6 +417,7 @@ Plan choose(Handle* h, int opa, int opb, int epi, long long M, long long N, long
     if (g_force_cfg < 0 && nn && g_mul == 3 && tma && K > 0 && c < FIRST_3M) continue;
     // operand-sum planes: only (and always) the sum-reading kernels; never without planes
     if (c >= FIRST_SUMS && !sums && g_force_cfg < 0) continue;
+    if (c >= FIRST_BSUMS && g_force_cfg < 0) continue;  // B-sum-only kernels: the width rule's
     if (g_force_cfg < 0 && sums && c < FIRST_SUMS) continue;
     const Entry& e = g_table[c][opa][opb][epi == EPI_FILTER ? EPI_FILTER : EPI_STORE];
     const Entry& ep = g_table[c][opa][opb][EPI_PARTIAL];
@@ -582,7 +603,10 @@ int run_kernel(Handle* h, int c, const Entry& e, dim3 grid, const GemmParams& p)
       CHFSI_TRY(encode_colmajor(&ma, p.A, p.M, p.K, p.lda, 8, kBKc[c]));
     CHFSI_TRY(encode_colmajor(&mb, p.B, p.K, p.N, p.ldb, kBKc[c], kBN[c]));
     if (c >= FIRST_SUMS) {
-      CHFSI_TRY(encode_sums_a(&ma, &mas, p, kBM[c], kBKc[c]));
+      if (c < FIRST_BSUMS)
+        CHFSI_TRY(encode_sums_a(&ma, &mas, p, kBM[c], kBKc[c]));
+      else
+        mas = ma;  // B-sum plane only (A is the 3-D box encoded above: sums imply M % 8 == 0)
       CHFSI_TRY(encode_real(&mbs, p.Bs, p.K, p.N, p.ldbs, kBKc[c], kBN[c], true));
     } else {
       mas = ma;

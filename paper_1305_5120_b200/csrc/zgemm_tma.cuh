@@ -95,10 +95,13 @@ __device__ __forceinline__ int perm8(int r) { return (r >> 1) | ((r & 1) << 2); 
 #endif
 constexpr int kDefer = CHFSI_TMA_DEFER;
 
+// operand-sum planes read by a 3M kernel: none (sums formed in the loop), both, B only
+constexpr int SUMS_NONE = 0, SUMS_BOTH = 1, SUMS_B = 2;
+
 // One k-tile sweep per stage: wait for the stage, run the BK/4 DMMA k-steps of the
 // warp tile, release the stage, and (rotating producer lane) refill the stage that
 // was released one iteration earlier.
-template <int BM, int BN, int WM, int WN, int STAGES, int MUL, bool SUMS, bool RAGGED, class Issue>
+template <int BM, int BN, int WM, int WN, int STAGES, int MUL, int SUMS, bool RAGGED, class Issue>
 __device__ __forceinline__ void tma_mainloop(const double2* sA,
                                              const double2* sB, const double* sAs,
                                              const double* sBs, uint64_t* full, uint64_t* empty,
@@ -123,8 +126,8 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
     // registers, shorter load-to-use latency)
     const unsigned a = smem_u32(sA + s * A_ELEMS);
     const unsigned b = smem_u32(sB + s * B_ELEMS);
-    const unsigned as_base = SUMS ? smem_u32(sAs + s * A_ELEMS) : 0u;
-    const unsigned bs_base = SUMS ? smem_u32(sBs + s * B_ELEMS) : 0u;
+    const unsigned as_base = SUMS == SUMS_BOTH ? smem_u32(sAs + s * A_ELEMS) : 0u;
+    const unsigned bs_base = SUMS != SUMS_NONE ? smem_u32(sBs + s * B_ELEMS) : 0u;
     #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       const int kk = ks * 4 + fc;
@@ -146,15 +149,20 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
         // 3M: three real products per complex MAC. The operand sums cost FM + FN DADDs
         // per 3 FM FN DMMAs.
         double as[FM], bs[FN];
-        if (SUMS) {
+        if (SUMS == SUMS_BOTH) {
           // precomputed operand sums: As [group][col][8 rows] (64 B per group column,
-          // rows permuted by column: sum_plane_grouped), Bs = {BK rows, BN cols} with
-          // 64-byte swizzle; both conflict-free per half-warp
+          // rows permuted by column: sum_plane_grouped), conflict-free per half-warp
           #pragma unroll
           for (int i = 0; i < FM; ++i) {
             const int mg = (wm * WM) / 8 + i;
             as[i] = lds64(as_base + 8u * (mg * 64 + kk * 8 + (pr ^ (((kk >> 1) & 1) << 1))));
           }
+        } else {
+          #pragma unroll
+          for (int i = 0; i < FM; ++i) as[i] = fa[i].x + fa[i].y;
+        }
+        if (SUMS != SUMS_NONE) {
+          // Bs = {BK rows, BN cols} with 64-byte swizzle (conflict-free per half-warp)
           #pragma unroll
           for (int j = 0; j < FN; ++j) {
             const int nn = wn * WN + j * 8 + pr;
@@ -162,8 +170,6 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
             bs[j] = lds64(bs_base + (off ^ (((off >> 7) & 3u) << 4)));
           }
         } else {
-          #pragma unroll
-          for (int i = 0; i < FM; ++i) as[i] = fa[i].x + fa[i].y;
           #pragma unroll
           for (int j = 0; j < FN; ++j) bs[j] = fb[j].x + fb[j].y;
         }
@@ -216,29 +222,33 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
   }
 }
 
-template <int BM, int BN, int WM, int WN, int STAGES, bool SUMS = false>
+template <int BM, int BN, int WM, int WN, int STAGES, int SUMS = SUMS_NONE>
 constexpr int zgemm_tma_smem_bytes() {
-  return STAGES * (BM * 8 + BN * 8) * (SUMS ? 24 : 16) + 1024 /* alignment slack */ +
-         2 * STAGES * 8;
+  return STAGES * (BM * 8 * (SUMS == SUMS_BOTH ? 24 : 16) + BN * 8 * (SUMS != SUMS_NONE ? 24 : 16)) +
+         1024 /* alignment slack */ + 2 * STAGES * 8;
 }
 
 // MUL = 4: four real products per complex MAC; MUL = 3: 3M. SUMS (3M only): the operand
 // sums Ar + Ai and Br + Bi arrive precomputed as real planes (p.As, p.Bs; maps mapAs,
 // mapBs), so the main loop issues no DADDs (an in-loop DADD stalls the DMMA stream:
-// ncu, DMMA pipe 88.6 % active with in-loop sums vs 95.8 % without).
+// ncu, DMMA pipe 88.6 % active with in-loop sums vs 95.8 % without). SUMS_B: only the
+// B plane is read (8 bytes per element of the narrow block); Ar + Ai is formed in the
+// loop, FM DADDs per 3 FM FN DMMAs, so H streams at 16 instead of 24 bytes per element:
+// the plan for narrow blocks, where the sum-plane kernel runs at the board's power cap.
 template <int BM, int BN, int WM, int WN, int STAGES, int EPI, int MINB = 1, int MUL = 4,
-          bool SUMS = false>
+          int SUMS = SUMS_NONE>
 __global__ void __launch_bounds__((BM / WM) * (BN / WN) * 32, MINB)
 zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapAs,
                  const __grid_constant__ CUtensorMap mapBs, const GemmParams p) {
-  static_assert(!SUMS || MUL == 3, "operand sums are a 3M feature");
+  static_assert(SUMS == SUMS_NONE || MUL == 3, "operand sums are a 3M feature");
   constexpr int BK = 8;
   constexpr int NWM = BM / WM;
   constexpr int NWARP = NWM * (BN / WN);
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
-  constexpr unsigned STAGE_BYTES = (A_ELEMS + B_ELEMS) * (SUMS ? 24 : 16);
+  constexpr unsigned STAGE_BYTES = A_ELEMS * (SUMS == SUMS_BOTH ? 24 : 16) +
+                                   B_ELEMS * (SUMS != SUMS_NONE ? 24 : 16);
   static_assert((A_ELEMS * 16) % 1024 == 0 && (B_ELEMS * 16) % 1024 == 0, "1 KB aligned tiles");
 
   extern __shared__ unsigned char smem_raw[];
@@ -246,10 +256,11 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double2* sA = base;
   double2* sB = base + STAGES * A_ELEMS;
-  double* sAs = reinterpret_cast<double*>(sB + STAGES * B_ELEMS);  // SUMS only
-  double* sBs = sAs + STAGES * A_ELEMS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(SUMS ? reinterpret_cast<void*>(sBs + STAGES * B_ELEMS)
-                                                    : reinterpret_cast<void*>(sAs));
+  double* sAs = reinterpret_cast<double*>(sB + STAGES * B_ELEMS);  // SUMS_BOTH only
+  double* sBs = sAs + (SUMS == SUMS_BOTH ? STAGES * A_ELEMS : 0);   // SUMS_BOTH / SUMS_B
+  uint64_t* full = reinterpret_cast<uint64_t*>(
+      SUMS != SUMS_NONE ? reinterpret_cast<void*>(sBs + STAGES * B_ELEMS)
+                        : reinterpret_cast<void*>(sAs));
   uint64_t* empty = full + STAGES;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -275,10 +286,10 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-    if (SUMS) {
+    if (SUMS == SUMS_BOTH)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapAs)) : "memory");
+    if (SUMS != SUMS_NONE)
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&mapBs)) : "memory");
-    }
   }
   __syncthreads();
 
@@ -288,12 +299,13 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     mbar_expect_tx(&full[s], STAGE_BYTES);
     // A: one {8 rows x BK cols} box per 8-row group (coords in doubles, columns);
     // B: one {BK rows x BN cols} box. Out-of-range rows/cols arrive zero-filled.
-    if (SUMS) {
+    if (SUMS != SUMS_NONE) {
       // four boxes per stage: A {16 doubles, BK cols, BM/8 groups} (M % 8 == 0), B, the
-      // grouped A-sum plane {8 rows, BK cols, BM/8 groups} and the B-sum plane
+      // grouped A-sum plane {8 rows, BK cols, BM/8 groups} and the B-sum plane (SUMS_B:
+      // three, no A-sum plane)
       tma_load_3d(sA + s * A_ELEMS, &mapA, 0, k0, m0 / 8, &full[s]);
       tma_load_2d(sB + s * B_ELEMS, &mapB, 2 * k0, n0, &full[s]);
-      tma_load_3d(sAs + s * A_ELEMS, &mapAs, 0, k0, m0 / 8, &full[s]);
+      if (SUMS == SUMS_BOTH) tma_load_3d(sAs + s * A_ELEMS, &mapAs, 0, k0, m0 / 8, &full[s]);
       tma_load_2d(sBs + s * B_ELEMS, &mapBs, k0, n0, &full[s]);
     } else {
       // A: one 3-D box when M % 8 == 0 (p.a3d, same smem layout), else BM/8 2-D boxes

@@ -415,9 +415,10 @@ def test_trtri_blocked_matches_inverse(eng):
 
 
 # every tile configuration and split factor the cost model can pick, on ragged shapes
-_NCFG = 17
+_NCFG = 19
 _TMA_FIRST = 7
 _SUMS_FIRST = 14  # 3M kernels reading operand-sum planes: filter calls only
+_BSUMS_FIRST = 17  # 3M kernels reading the B-sum plane only (narrow blocks)
 
 
 @pytest.mark.parametrize("cfg", list(range(_SUMS_FIRST)))
@@ -454,7 +455,8 @@ def test_every_gemm_config_and_split(eng, cfg, split):
         lib.chfsi_gemm_override(-1, 0)
 
 
-@pytest.mark.parametrize("cfg", [-1, _SUMS_FIRST, _SUMS_FIRST + 1, _SUMS_FIRST + 2, 7, 11])
+@pytest.mark.parametrize("cfg", [-1, _SUMS_FIRST, _SUMS_FIRST + 1, _SUMS_FIRST + 2, _BSUMS_FIRST,
+                                 _BSUMS_FIRST + 1, 7, 11])
 @pytest.mark.parametrize("split", [0, 1, 3])
 def test_filter_with_sum_planes(eng, cfg, split):
     """chfsi_filter with 3M operand-sum planes (Hs, and per block the plane its step's
@@ -505,12 +507,12 @@ def test_filter_width_rule_large_operator(eng):
             cfg, split = ctypes.c_int(), ctypes.c_int()
             _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg),
                          ctypes.byref(split))
-            # one 32-column tile (17-32 columns): the in-loop-sum 3M kernel (cfg 11),
-            # which does not stream H's sum plane (the power-capped regime, zgemm.cu)
-            if 16 < k <= 32:
-                assert cfg.value == 11, (k, cfg.value)
+            # narrow blocks: the B-sum-only 3M kernels (cfg 17 / 18), which do not stream
+            # H's sum plane (the power-capped regime, zgemm.cu)
+            if 16 < k <= 64:
+                assert cfg.value >= _BSUMS_FIRST, (k, cfg.value)
             else:
-                assert cfg.value >= _SUMS_FIRST, (k, cfg.value)
+                assert _SUMS_FIRST <= cfg.value < _BSUMS_FIRST, (k, cfg.value)
             Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
             W = torch.empty_like(Y)
             a, b, lam_ref = -1.0, 1.0, -2.0
