@@ -34,7 +34,7 @@ for cfg in range(14):
                           D.to_device(B, eng.device), 0.5, C)
 lib.chfsi_gemm_override(-1, 0)
 # sum-plane filter configs (n % 8 == 0), ragged widths, forced splits
-for cfg in (14, 15, 16, -1):
+for cfg in (14, 15, 16, 17, 18, -1):  # 17 / 18: the B-sum-only kernels
     for split in (1, 3, 0):
         lib.chfsi_gemm_override(cfg, split)
         for (n, k) in [(136, 5), (64, 37), (200, 26)]:
@@ -58,8 +58,9 @@ eng.declare_operator(None)
 Hbig = torch.randn((8192, 8192), dtype=torch.complex128, device=eng.device)
 eng.filter(Hbig, torch.randn((26, 8192), dtype=torch.complex128, device=eng.device),
            torch.empty((26, 8192), dtype=torch.complex128, device=eng.device), 2, -1.0, 1.0, -2.0)
-# round 2: the narrow rule's in-loop kernel (17-32 columns) and a two-tile block
-for kk in (20, 40):
+# round 2: the narrow rule's B-sum-only kernels (17-64 columns: one and two tiles, 24-
+# and 32-wide) and a block just past the rule
+for kk in (20, 40, 51, 70):
     eng.filter(Hbig, torch.randn((kk, 8192), dtype=torch.complex128, device=eng.device),
                torch.empty((kk, 8192), dtype=torch.complex128, device=eng.device), 2, -1.0, 1.0,
                -2.0)
