@@ -641,6 +641,11 @@ int launch(Handle* h, int opa, int opb, int epi, long long M, long long N, long 
   const Plan pl = cached_plan(h, opa, opb, epi, M, N, K, sums, tma);
   const int c = pl.cfg;
   p.a3d = (M % 8 == 0) ? 1 : 0;  // one 3-D A box per stage (TMA kernels)
+  static const int pack_tail = [] {
+    const char* e = getenv("CHFSI_PACK_TAIL");  // tuning only
+    return (e && atoi(e) == 0) ? 0 : 1;
+  }();
+  p.pack = pack_tail;
   if (c >= FIRST_SUMS && !sums) {
     set_error("zgemm: forced config " + std::to_string(c) + " needs operand sum planes");
     return ERR_ARG;

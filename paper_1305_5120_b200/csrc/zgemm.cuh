@@ -58,6 +58,9 @@ struct GemmParams {
   // step's Bs
   // TMA kernels: A arrives as one 3-D box per stage (M % 8 == 0), set by the launcher
   int a3d;
+  // 3M TMA kernels: a last live 8-column block holding <= 4 columns is multiplied in the
+  // packed four-product form (zgemm_tma.cuh); set by the launcher (CHFSI_PACK_TAIL=0: off)
+  int pack;
   const double* As; long long ldas;
   const double* Bs; long long ldbs;
   double* Cs; long long ldcs;

@@ -101,7 +101,12 @@ constexpr int SUMS_NONE = 0, SUMS_BOTH = 1, SUMS_B = 2;
 // One k-tile sweep per stage: wait for the stage, run the BK/4 DMMA k-steps of the
 // warp tile, release the stage, and (rotating producer lane) refill the stage that
 // was released one iteration earlier.
-template <int BM, int BN, int WM, int WN, int STAGES, int MUL, int SUMS, bool RAGGED, class Issue>
+// TAIL: 0 interior warp tile (every 8-column block live), 1 ragged (blocks >= jvalid are
+// skipped), 2 ragged with a PACKED last live block (3M only): a block holding at most 4
+// real columns is multiplied as the real 8-column operand [Re y_0..3 | Im y_0..3], two
+// DMMAs per row group (Ar x, Ai x) instead of 3M's three -- the block of a 26-column
+// shard that holds 2 columns costs 2/3 of a padded one (8 % of that shard's step).
+template <int BM, int BN, int WM, int WN, int STAGES, int MUL, int SUMS, int TAIL, int JV, class Issue>
 __device__ __forceinline__ void tma_mainloop(const double2* sA,
                                              const double2* sB, const double* sAs,
                                              const double* sBs, uint64_t* full, uint64_t* empty,
@@ -114,6 +119,12 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
   constexpr int NWARP = (BM / WM) * (BN / WN);
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
+  constexpr bool RAGGED = TAIL != 0;
+  // TAIL == 2: the live-block count is the compile-time JV (one instantiation per count),
+  // so the packed block's operands are fixed registers, not run-time selects
+  constexpr int jpack = (TAIL == 2) ? JV - 1 : -1;
+  if (TAIL == 2) jvalid = JV;
+  const int q = lane >> 2;
   // unrolled by the ring depth: the stage index, its smem addresses and barrier slots
   // become compile-time constants in each copy (ncu: DMMA pipe 95.5 -> 97.4 % for the
   // sum-plane filter kernel, 47.1 -> 48.2 TF/s at k = 2200)
@@ -142,8 +153,16 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
       }
       #pragma unroll
       for (int j = 0; j < FN; ++j) {
-        const int nn = wn * WN + j * 8 + pr;
-        fb[j] = lds128(b + 16u * (nn * 8 + (kk ^ pr)));
+        if (TAIL == 2 && j == jpack) {
+          // packed block: fragment column q <- Re (q < 4) or Im (q >= 4) of tile column q & 3
+          const int nn = wn * WN + j * 8 + (q & 3);
+          const double2 v = lds128(b + 16u * (nn * 8 + (kk ^ (q & 3))));
+          fb[j].x = (q < 4) ? v.x : v.y;
+          fb[j].y = 0.0;
+        } else {
+          const int nn = wn * WN + j * 8 + pr;
+          fb[j] = lds128(b + 16u * (nn * 8 + (kk ^ pr)));
+        }
       }
       if (MUL == 3) {
         // 3M: three real products per complex MAC. The operand sums cost FM + FN DADDs
@@ -178,14 +197,17 @@ __device__ __forceinline__ void tma_mainloop(const double2* sA,
           #pragma unroll
           for (int j = 0; j < FN; ++j)
             if (!RAGGED || j < jvalid) {
+              // (packed block: c0 = Ar [yr | yi], c1 = Ai [yr | yi])
               dmma884(c0[i][j][0], c0[i][j][1], fa[i].x, fb[j].x);
-              dmma884(c1[i][j][0], c1[i][j][1], fa[i].y, fb[j].y);
+              dmma884(c1[i][j][0], c1[i][j][1], fa[i].y,
+                      (TAIL == 2 && j == jpack) ? fb[j].x : fb[j].y);
             }
         #pragma unroll
         for (int i = 0; i < FM; ++i)
           #pragma unroll
           for (int j = 0; j < FN; ++j)
-            if (!RAGGED || j < jvalid) dmma884(c2[i][j][0], c2[i][j][1], as[i], bs[j]);
+            if ((!RAGGED || j < jvalid) && !(TAIL == 2 && j == jpack))
+              dmma884(c2[i][j][0], c2[i][j][1], as[i], bs[j]);
       } else {
         // two sweeps over the warp tile: the second update of each accumulator is
         // 2*FM*FN DMMAs after the first, so no DMMA waits on its predecessor
@@ -242,6 +264,11 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
                  const __grid_constant__ CUtensorMap mapAs,
                  const __grid_constant__ CUtensorMap mapBs, const GemmParams p) {
   static_assert(SUMS == SUMS_NONE || MUL == 3, "operand sums are a 3M feature");
+  // packed tail blocks: the narrow-block kernels (B-sum plane only). Measured A/B on one
+  // B200, sustained degree-25 calls at n = 20000: k = 26 2.303 -> 2.184 ms, k = 51 4.10 ->
+  // 4.03 ms; in the both-plane kernels (k = 201, 210) it was -1 % / +0.4 % at the power
+  // cap, so they keep the plain ragged path.
+  constexpr bool PACK_TAIL = (MUL == 3 && SUMS == SUMS_B);
   constexpr int BK = 8;
   constexpr int NWM = BM / WM;
   constexpr int NWARP = NWM * (BN / WN);
@@ -343,11 +370,43 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       #pragma unroll
       for (int t = 0; t < 2; ++t) c0[i][j][t] = c1[i][j][t] = c2[i][j][t] = 0.0;
 
-  if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, false>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
+  // 3M: a last live block with at most 4 real columns is packed (TAIL = 2 above)
+  const int last_cols = p.N - (n0 + wn * WN + (jvalid - 1) * 8);  // of block jvalid - 1
+  const bool packed = MUL == 3 && PACK_TAIL && p.pack && jvalid >= 1 && last_cols <= 4;
+  const int jpack = packed ? jvalid - 1 : -1;
+  if (packed) {
+    constexpr int TP = (MUL == 3 && PACK_TAIL) ? 2 : 1;
+    #define CHFSI_PACKED_LOOP(JV_)                                                              \
+      tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, TP, JV_>(sA, sB, sAs, sBs, full, empty,   \
+                                                               issue, KT, wm, wn, lane, warp,   \
+                                                               fc, pr, jvalid, c0, c1, c2)
+    if (FN >= 4 && jvalid == 4) CHFSI_PACKED_LOOP(4);
+    else if (FN >= 3 && jvalid == 3) CHFSI_PACKED_LOOP(3);
+    else if (FN >= 2 && jvalid == 2) CHFSI_PACKED_LOOP(2);
+    else CHFSI_PACKED_LOOP(1);
+    #undef CHFSI_PACKED_LOOP
+    // fragment columns 0-3 hold the products with Re y, 4-7 with Im y: lanes fc < 2 take
+    // the other half from lane ^ 2 and form Re = Ar yr - Ai yi, Im = Ar yi + Ai yr
+    #pragma unroll
+    for (int i = 0; i < FM; ++i)
+      #pragma unroll
+      for (int j = 0; j < FN; ++j)
+        if (j == jpack) {
+          #pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const double o1 = __shfl_xor_sync(0xffffffffu, c0[i][j][t], 2);
+            const double o2 = __shfl_xor_sync(0xffffffffu, c1[i][j][t], 2);
+            const double re = __dsub_rn(c0[i][j][t], o2);
+            const double im = __dadd_rn(o1, c1[i][j][t]);
+            c0[i][j][t] = re;
+            c1[i][j][t] = im;
+          }
+        }
+  } else if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, 0, 0>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                     lane, warp, fc, pr, jvalid, c0, c1, c2);
   } else {  // ragged column edge: skip 8-column blocks past N
-    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, true>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
+    tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, 1, 0>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                    lane, warp, fc, pr, jvalid, c0, c1, c2);
   }
 
@@ -360,13 +419,18 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
     for (int j = 0; j < FN; ++j) {
       #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        const int n = n0 + wn * WN + j * 8 + perm8(fc * 2 + t);
-        if (n >= p.N) continue;
+        const bool pk = (j == jpack);  // packed block: columns in fragment order, fc < 2
+        const int n = n0 + wn * WN + j * 8 + (pk ? fc * 2 + t : perm8(fc * 2 + t));
+        if (n >= p.N || (pk && fc >= 2)) continue;
         // explicit roundings (no contraction choices left to the compiler): every
         // instantiation -- tile shape, sum planes or not -- rounds the same way, so a
         // product is bit-identical whichever config the planner picks without split-K
+        // (a packed tail block is a four-product result: same inputs, its own rounding)
         double xr, xi;
-        if (MUL == 3) {
+        if (pk) {
+          xr = c0[i][j][t];
+          xi = c1[i][j][t];
+        } else if (MUL == 3) {
           xr = __dsub_rn(c0[i][j][t], c1[i][j][t]);
           xi = __dsub_rn(__dsub_rn(c2[i][j][t], c0[i][j][t]), c1[i][j][t]);
         } else {

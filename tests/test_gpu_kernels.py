@@ -462,7 +462,8 @@ def test_filter_with_sum_planes(eng, cfg, split):
     """chfsi_filter with 3M operand-sum planes (Hs, and per block the plane its step's
     epilogue or split-K reduce wrote): every sum-reading config and split against the
     oracle recurrence, ragged n and k; a forced config that reads no planes (7, 11) still
-    leaves correct planes for the next step (separate sum pass)."""
+    leaves correct planes for the next step (separate sum pass); the B-sum-only configs
+    (17, 18) with their packed tail blocks."""
     import oracle.chfsi_oracle as O
     from paper_1305_5120_b200 import _native, device as D
     from paper_1305_5120_b200.workloads import baseline_matrix
@@ -473,6 +474,11 @@ def test_filter_with_sum_planes(eng, cfg, split):
         sizes = [(304, 37, 6), (1000, 120, 5), (136, 1, 3), (8, 1, 4), (16, 3, 2), (24, 40, 3)]
         if cfg < _SUMS_FIRST:
             sizes.append((301, 37, 6))
+        if cfg >= _BSUMS_FIRST:
+            # packed tail block (last live 8-column block with 1-4 columns) at every live
+            # block count of a 32- and a 24-wide tile, and the unpacked 5-column tail
+            sizes += [(64, 26, 3), (200, 20, 3), (72, 12, 2), (128, 33, 2), (128, 28, 2),
+                      (128, 4, 2), (128, 29, 2)]
         for (n, k, m) in sizes:
             h, lam, _ = baseline_matrix(n, n)
             rng = np.random.default_rng(n + k + cfg)
