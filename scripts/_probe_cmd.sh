@@ -1,5 +1,4 @@
 set -x
-mkdir -p gpurun_out/s10
-(time timeout 2400 python -m pytest tests -m gpu -x -q) > gpurun_out/s10/pytest.log 2>&1; echo rc=$?
-tail -5 gpurun_out/s10/pytest.log
-timeout 900 python scripts/rank_phase_probe.py > gpurun_out/s10/rank_phases.json 2> gpurun_out/s10/rank_phases.err; echo rc=$?
+mkdir -p gpurun_out/s11
+(time python bench.py --impl reference --gpus 1 --steps 20 --warmup 5) > gpurun_out/s11/bench_ref.log 2>&1; echo ref_rc=$?
+(time python bench.py --gpus 1 --steps 20 --warmup 5) > gpurun_out/s11/bench.log 2>&1; echo bench_rc=$?
