@@ -961,7 +961,9 @@ def tail_widths(eng, H, n, dev, a_edge, b_up, lam_ref, degree=5):
     import torch
     out = {}
     eng.declare_operator(H)  # as in a solve: H's 3M sum plane formed once, not per call
-    for k in (26, 210, 275):
+    # 26 / 51 / 101: the 8- / 4- / 2-GPU shards of the reference-interval tail block
+    # (k_a = 201); 210: that tail on one GPU; 275: the 8-GPU shard of the full block
+    for k in (26, 51, 101, 210, 275):
         Y0 = torch.randn((k, n), dtype=torch.complex128, device=dev)
         Y = torch.empty_like(Y0)
         W = torch.empty_like(Y)
