@@ -509,7 +509,9 @@ def test_filter_width_rule_large_operator(eng):
     H = H.contiguous()
     eng.declare_operator(H)
     try:
-        for k in (1, 8, 26, 40, 51, 100, 101, 201, 550):
+        # (20 / 25 / 28 / 33 / 42 / 57 / 60: packed tail blocks of 1-4 columns at every
+        # live-block count of the 32- and 24-wide narrow kernels)
+        for k in (1, 8, 20, 25, 26, 28, 33, 40, 42, 51, 57, 60, 100, 101, 201, 550):
             cfg, split = ctypes.c_int(), ctypes.c_int()
             _native.call("chfsi_gemm_plan", eng.h, 0, 0, 2, n, k, n, ctypes.byref(cfg),
                          ctypes.byref(split))
@@ -530,6 +532,13 @@ def test_filter_width_rule_large_operator(eng):
             ref2 = (2 * s2 / e) * (ref1 @ H - c * ref1) - s1 * s2 * Y
             out = eng.filter(H, Y.clone(), W, 2, a, b, lam_ref)
             err = float(torch.linalg.norm(out - ref2) / torch.linalg.norm(ref2))
+            assert err <= 1e-13, (k, err)
+            # the Rayleigh-Ritz product H Q on the declared operator takes the same plans
+            # with the plain store epilogue
+            HQ = torch.empty_like(Y)
+            eng.apply_operator(H, Y, HQ)
+            ref = Y @ H
+            err = float(torch.linalg.norm(HQ - ref) / torch.linalg.norm(ref))
             assert err <= 1e-13, (k, err)
     finally:
         eng.declare_operator(None)

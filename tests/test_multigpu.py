@@ -299,6 +299,32 @@ def test_in_process_solve_two_ranks_and_default_devices():
 
 
 @pytest.mark.gpu
+def test_in_process_solve_eight_ranks_ragged_and_empty_shards():
+    """The north star's rank count: 8 rank threads (sharing cuda:0 here) on a problem whose
+    active block shrinks below 8 columns before it converges (nev + nex = 13: shards of 2
+    and 1 columns from the start, empty shards at the end), standard and generalized."""
+    import oracle.chfsi_oracle as O
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_matrix
+    h, lam_true, _ = baseline_matrix(31, 200)
+    cfg = G.SolverConfig(nev=10, buffer=3, degree=12, max_outer_iters=4000)
+    lam1, v1, rep1 = G.chfsi_solve(h, None, cfg, seed=7)
+    lam8, v8, rep8 = G.chfsi_solve(h, None, cfg, seed=7, devices=[0] * 8)
+    assert rep8.converged and rep1.converged and len(lam8) == len(lam1) == cfg.nev
+    assert np.max(np.abs(lam8 - lam1) / np.abs(lam1)) <= 1e-10
+    assert O.largest_angle_sine(v8.entries, v1.entries) < 1e-8
+    assert float(G.residuals(h, v8, lam8).max()) < cfg.tol
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((200, 200)) + 1j * rng.standard_normal((200, 200))
+    b = np.eye(200) + 0.1 * (b.conj().T @ b) / np.linalg.norm(b.conj().T @ b, 2)
+    g1, c1, _ = G.solve_generalized(h, b, None, cfg, seed=7)
+    g8, c8, _ = G.solve_generalized(h, b, None, cfg, seed=7, devices=[0] * 8)
+    assert np.max(np.abs(g8 - g1) / np.abs(g1)) <= 1e-10
+    gram = c8.entries.conj().T @ b @ c8.entries
+    assert np.linalg.norm(gram - np.eye(cfg.nev)) <= 1e-9
+
+
+@pytest.mark.gpu
 def test_in_process_guard_fails_cleanly_on_divergent_rank():
     """Fault injection: rank 1's gathered Rayleigh-Ritz Gram gets a one-ulp change.
     Every rank must raise ChfsiError (cross-rank divergence), not hang."""
