@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--legs", default="",
                     help="comma list: run only these extra legs (development; default all)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--time-budget-s", type=float, default=840.0,
+    ap.add_argument("--time-budget-s", type=float, default=720.0,
                     help="an optional leg is skipped (and says so in the line) when the "
                          "process has already run this long minus the leg's usual duration, "
                          "so the JSON line is printed before any outer limit")
