@@ -544,6 +544,36 @@ def test_filter_width_rule_large_operator(eng):
         eng.declare_operator(None)
 
 
+def test_narrow_kernels_every_width(eng):
+    """Every block width the narrow-block rule takes (17-64 columns: 32- and 24-wide tiles,
+    each live-block count, packed and plain tail blocks), one fused degree step and one
+    split-K plan each, against a torch (cuBLAS ZGEMM) product."""
+    import torch
+    n = 8192
+    dev = eng.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    H = torch.randn((n, n), dtype=torch.complex128, device=dev, generator=g)
+    H = ((H + H.mH) * 0.5).contiguous()
+    eng.declare_operator(H)
+    try:
+        for k in range(17, 65):
+            Y = torch.randn((k, n), dtype=torch.complex128, device=dev, generator=g)
+            W = torch.empty_like(Y)
+            a, b, lam_ref = -1.0, 1.0, -2.0
+            c, e = (a + b) / 2, (b - a) / 2
+            s1 = e / (lam_ref - c)
+            ref = (s1 / e) * (Y @ H - c * Y)
+            out = eng.filter(H, Y.clone(), W, 1, a, b, lam_ref)
+            err = float(torch.linalg.norm(out - ref) / torch.linalg.norm(ref))
+            assert err <= 1e-13, (k, err)
+            # column by column too: a wrong pairing in a packed block would hide in a norm
+            cerr = torch.linalg.norm(out - ref, dim=1) / torch.linalg.norm(ref, dim=1)
+            assert float(cerr.max()) <= 1e-13, (k, int(cerr.argmax()), float(cerr.max()))
+    finally:
+        eng.declare_operator(None)
+
+
 @pytest.mark.parametrize("declared", [False, True])
 def test_filter_sum_planes_with_padded_leading_dims(eng, declared):
     """Sum-plane filter steps on views with ld > n (H, Y and W inside larger buffers):
