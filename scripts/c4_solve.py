@@ -44,6 +44,10 @@ def main():
     ap.add_argument("--generalized", action="store_true")
     ap.add_argument("--max-it", type=int, default=20000)
     ap.add_argument("--out", default="gpurun_out/c4.json")
+    ap.add_argument("--ranks", type=int, default=1,
+                    help="column-shard every solve over this many in-process ranks "
+                         "(devices=[0] * ranks: rank threads sharing cuda:0 -- a check of "
+                         "the N-rank code path at full size, not a timing)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     eng = D.Engine.get(dev)
@@ -67,7 +71,8 @@ def main():
                          max_outer_iters=args.max_it, interval=args.interval)
     results = {"n": n, "nev": args.nev, "nex": args.nex, "degree": args.degree,
                "interval": args.interval, "generalized": args.generalized, "t_generate_s": t_gen,
-               "problems": []}
+               "ranks": args.ranks, "problems": []}
+    shard = {"devices": [0] * args.ranks} if args.ranks > 1 else {}
     prev, prior, running = None, None, None
     smat = G.HermitianDenseMatrix.from_device(s, trusted=True) if s is not None else None
     gE = torch.Generator(device=dev)
@@ -104,10 +109,10 @@ def main():
         try:
             if smat is None:
                 lamc, vecs, rep = G.chfsi_solve(amat, y0, cfg, prior=prior, seed=solver_rng,
-                                                callback=log)
+                                                callback=log, **shard)
             else:
                 lamc, vecs, rep = G.solve_generalized(amat, smat, y0, cfg, prior=prior,
-                                                      seed=solver_rng, callback=log)
+                                                      seed=solver_rng, callback=log, **shard)
         except G.NotConverged as exc:
             rep = exc.report
             results["problems"].append({
