@@ -22,6 +22,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "zgemm.cuh"
 
 namespace chfsi {
@@ -370,38 +372,44 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       #pragma unroll
       for (int t = 0; t < 2; ++t) c0[i][j][t] = c1[i][j][t] = c2[i][j][t] = 0.0;
 
-  // 3M: a last live block with at most 4 real columns is packed (TAIL = 2 above)
-  const int last_cols = p.N - (n0 + wn * WN + (jvalid - 1) * 8);  // of block jvalid - 1
-  const bool packed = MUL == 3 && PACK_TAIL && p.pack && jvalid >= 1 && last_cols <= 4;
-  const int jpack = packed ? jvalid - 1 : -1;
-  if (packed) {
-    constexpr int TP = (MUL == 3 && PACK_TAIL) ? 2 : 1;
-    #define CHFSI_PACKED_LOOP(JV_)                                                              \
-      tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, TP, JV_>(sA, sB, sAs, sBs, full, empty,   \
-                                                               issue, KT, wm, wn, lane, warp,   \
-                                                               fc, pr, jvalid, c0, c1, c2)
-    if (FN >= 4 && jvalid == 4) CHFSI_PACKED_LOOP(4);
-    else if (FN >= 3 && jvalid == 3) CHFSI_PACKED_LOOP(3);
-    else if (FN >= 2 && jvalid == 2) CHFSI_PACKED_LOOP(2);
-    else CHFSI_PACKED_LOOP(1);
-    #undef CHFSI_PACKED_LOOP
-    // fragment columns 0-3 hold the products with Re y, 4-7 with Im y: lanes fc < 2 take
-    // the other half from lane ^ 2 and form Re = Ar yr - Ai yi, Im = Ar yi + Ai yr
-    #pragma unroll
-    for (int i = 0; i < FM; ++i)
+  // 3M narrow-block kernels: a last live block with at most 4 real columns is packed
+  // (TAIL = 2 above); warp-uniform
+  int jpack = -1;
+  if constexpr (PACK_TAIL) {
+    const int last_cols = p.N - (n0 + wn * WN + (jvalid - 1) * 8);  // of block jvalid - 1
+    if (p.pack && jvalid >= 1 && last_cols <= 4) jpack = jvalid - 1;
+  }
+  if (jpack >= 0) {
+    if constexpr (PACK_TAIL) {
+      // one main-loop instantiation per live-block count: the packed block's operands are
+      // fixed registers
+      auto run = [&](auto jv) {
+        tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, 2, decltype(jv)::value>(
+            sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn, lane, warp, fc, pr, jvalid, c0, c1,
+            c2);
+      };
+      if (FN >= 4 && jvalid == 4) run(std::integral_constant<int, (FN >= 4 ? 4 : 1)>{});
+      else if (FN >= 3 && jvalid == 3) run(std::integral_constant<int, (FN >= 3 ? 3 : 1)>{});
+      else if (FN >= 2 && jvalid == 2) run(std::integral_constant<int, (FN >= 2 ? 2 : 1)>{});
+      else run(std::integral_constant<int, 1>{});
+      // fragment columns 0-3 hold the products with Re y, 4-7 with Im y: lanes fc < 2 take
+      // the other half from lane ^ 2 and form Re = Ar yr - Ai yi, Im = Ar yi + Ai yr
       #pragma unroll
-      for (int j = 0; j < FN; ++j)
-        if (j == jpack) {
-          #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const double o1 = __shfl_xor_sync(0xffffffffu, c0[i][j][t], 2);
-            const double o2 = __shfl_xor_sync(0xffffffffu, c1[i][j][t], 2);
-            const double re = __dsub_rn(c0[i][j][t], o2);
-            const double im = __dadd_rn(o1, c1[i][j][t]);
-            c0[i][j][t] = re;
-            c1[i][j][t] = im;
+      for (int i = 0; i < FM; ++i)
+        #pragma unroll
+        for (int j = 0; j < FN; ++j)
+          if (j == jpack) {
+            #pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const double o1 = __shfl_xor_sync(0xffffffffu, c0[i][j][t], 2);
+              const double o2 = __shfl_xor_sync(0xffffffffu, c1[i][j][t], 2);
+              const double re = __dsub_rn(c0[i][j][t], o2);
+              const double im = __dadd_rn(o1, c1[i][j][t]);
+              c0[i][j][t] = re;
+              c1[i][j][t] = im;
+            }
           }
-        }
+    }
   } else if (jvalid == FN) {  // interior warp tile: unconditional DMMA stream
     tma_mainloop<BM, BN, WM, WN, STAGES, MUL, SUMS, 0, 0>(sA, sB, sAs, sBs, full, empty, issue, KT, wm, wn,
                                                     lane, warp, fc, pr, jvalid, c0, c1, c2);

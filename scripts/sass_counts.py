@@ -20,11 +20,12 @@ for b in blocks[1:]:
     if "zgemm_tma_kernel" not in name and "zgemv" not in name:
         continue
     counts = {op: len(re.findall(r"\b" + op + r"[\.\s]", b)) for op in OPS}
-    m = re.search(r"zgemm_tma_kernelILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELb(\d)E", name)
+    m = re.search(r"zgemm_tma_kernelILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d)E", name)
     if m:
         bm, bn, wm, wn, st, epi, _, mul, sums = (int(x) for x in m.groups())
         label = (f"zgemm_tma<{bm}x{bn}, warp {wm}x{wn}, {st} stages, epi={EPI.get(epi, epi)}, "
-                 f"{'3M' if mul == 3 else '4 products'}{', sum planes' if sums else ''}>")
+                 f"{'3M' if mul == 3 else '4 products'}"
+                 f"{['', ', sum planes', ', B-sum plane only + packed tail block'][sums]}>")
     else:
         label = name[:80]
     print(label + " | " + " | ".join(str(counts[op]) for op in OPS))
