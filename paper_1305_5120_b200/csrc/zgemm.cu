@@ -257,6 +257,8 @@ struct Plan {
   int cfg = 0;
   int split = 1;
   int k_chunk = 0;
+  // mixed tiling (cfg 15 only): n_wide 32-column tiles, then n_narrow 24-column tiles
+  int n_wide = 0, n_narrow = 0;
 };
 
 // Launch-time model (microseconds), fitted by scripts/fit_cost_model.py to 2900
@@ -349,6 +351,13 @@ long long bsums_max_n() {
   }();
   return v;
 }
+bool mixed_tiles() {
+  static const bool on = [] {
+    const char* e = getenv("CHFSI_MIXED_TILES");  // tuning only
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
 bool narrow_inloop(long long N) {
   static const bool on = [] {
     const char* e = getenv("CHFSI_NARROW_INLOOP");
@@ -383,7 +392,29 @@ Plan choose_sums_rule(long long M, long long N, long long K) {
       best.cfg = c;
     }
   }
-  const long long tn = (N + kBN[best.cfg] - 1) / kBN[best.cfg];
+  // Mixed tiling: 8 m columns of DMMA work are covered exactly by a 32-column and b
+  // 24-column tiles of the row-stacked 32-wide kernel (cfg 15: every warp spans the tile's
+  // columns, so a 24-column tile keeps 3 live blocks in every warp) in one launch --
+  // no ragged last tile, whose loads cost >= 0.86 of a full tile whatever it holds.
+  if (!bonly && mixed_tiles()) {
+    const long long m8 = (N + 7) / 8;
+    for (long long b = 1; b <= 3; ++b) {
+      const long long rest = m8 - 3 * b;
+      if (rest < 0 || rest % 4 != 0) continue;
+      const long long a = rest / 4;
+      if (a < 1) break;  // 24-column tiles only: cfg 16 is that plan
+      const double score = (double)(8 * m8) * 1.004 * (1.0 + 0.02 * (double)b / (double)(a + b));
+      if (score < best_score) {
+        best_score = score;
+        best.cfg = FIRST_SUMS + 1;
+        best.n_wide = (int)a;
+        best.n_narrow = (int)b;
+      }
+      break;
+    }
+  }
+  const long long tn = best.n_narrow > 0 ? best.n_wide + best.n_narrow
+                                         : (N + kBN[best.cfg] - 1) / kBN[best.cfg];
   const long long ktiles = std::max<long long>(1, (K + 7) / 8);
   const long long ws_cap = std::max<long long>(1, (1LL << 30) / std::max<long long>(1, M * N * 16));
   // (narrow kernels on two column tiles: split 24 measured 1.6 % ahead of 16 at k = 51)
@@ -673,6 +704,11 @@ int launch_plan(Handle* h, int opa, int opb, int epi, long long M, long long N, 
   const int c = pl.cfg;
   p.tiles_m = (int)((M + kBM[c] - 1) / kBM[c]);
   p.tiles_n = (int)((N + kBN[c] - 1) / kBN[c]);
+  p.n_wide = 0;
+  if (pl.n_narrow > 0) {  // mixed tiling: n_wide full tiles, then n_narrow of BN - 8 columns
+    p.n_wide = pl.n_wide;
+    p.tiles_n = pl.n_wide + pl.n_narrow;
+  }
   // Row-major raster (consecutive CTAs share one H row strip). A grouped raster
   // (several row tiles per wave sharing Y strips) measured 1.5 % slower on B200
   // with the cp.async kernel (profiles/r01), so group = 1 unless CHFSI_RASTER_GROUP

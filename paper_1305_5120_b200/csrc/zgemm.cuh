@@ -61,6 +61,10 @@ struct GemmParams {
   // 3M TMA kernels: a last live 8-column block holding <= 4 columns is multiplied in the
   // packed four-product form (zgemm_tma.cuh); set by the launcher (CHFSI_PACK_TAIL=0: off)
   int pack;
+  // TMA kernels with one warp column (WN == BN): the first n_wide column tiles are BN wide,
+  // the rest BN - 8 (their last 8-column block is skipped), so 32- and 24-column tiles
+  // cover a block of 8 m columns exactly in one launch; 0: every tile BN wide
+  int n_wide;
   const double* As; long long ldas;
   const double* Bs; long long ldbs;
   double* Cs; long long ldcs;

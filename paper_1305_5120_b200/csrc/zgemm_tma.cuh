@@ -296,7 +296,18 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   const int wm = warp % NWM, wn = warp / NWM;
   int mi, ni;
   tile_coords(p, blockIdx.x, mi, ni);
-  const int m0 = mi * BM, n0 = ni * BN;
+  const int m0 = mi * BM;
+  // column tile [n0, nend): BN wide, or (mixed tiling, GemmParams::n_wide) BN - 8 wide
+  // after the first n_wide tiles
+  // (only the kernels whose warps span the tile's columns compile it: a narrower tile
+  // keeps the same live blocks in every warp)
+  int n0 = ni * BN, nend = p.N;
+  if constexpr (WN == BN && BN == 32) {
+    if (p.n_wide > 0) {
+      n0 = (ni < p.n_wide) ? ni * BN : p.n_wide * BN + (ni - p.n_wide) * (BN - 8);
+      nend = min(p.N, n0 + ((ni < p.n_wide) ? BN : BN - 8));
+    }
+  }
   if ((p.tri & TRI_C_LOWER) && m0 + BM <= n0) return;  // strictly upper tile (CTA-uniform)
   int kbeg = 0, kend = p.K;
   if (EPI == EPI_PARTIAL) {
@@ -360,7 +371,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   // 8-column MMA blocks of this warp that hold at least one real column: blocks
   // entirely past N (the padded tail of a narrow filter block) issue no DMMAs.
   // Warp-uniform, so DMMA's warp-collective semantics are kept.
-  const int jvalid = min(FN, max(0, (p.N - (n0 + wn * WN) + 7) / 8));
+  const int jvalid = min(FN, max(0, (nend - (n0 + wn * WN) + 7) / 8));
   // MUL == 4: c0 = Re, c1 = Im, four real products per complex MAC.
   // MUL == 3: c0 = Ar Br, c1 = Ai Bi, c2 = (Ar + Ai)(Br + Bi) (3M); the epilogue forms
   // Re = c0 - c1, Im = c2 - c0 - c1.
@@ -376,7 +387,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   // (TAIL = 2 above); warp-uniform
   int jpack = -1;
   if constexpr (PACK_TAIL) {
-    const int last_cols = p.N - (n0 + wn * WN + (jvalid - 1) * 8);  // of block jvalid - 1
+    const int last_cols = nend - (n0 + wn * WN + (jvalid - 1) * 8);  // of block jvalid - 1
     if (p.pack && jvalid >= 1 && last_cols <= 4) jpack = jvalid - 1;
   }
   if (jpack >= 0) {
@@ -429,7 +440,7 @@ zgemm_tma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       for (int t = 0; t < 2; ++t) {
         const bool pk = (j == jpack);  // packed block: columns in fragment order, fc < 2
         const int n = n0 + wn * WN + j * 8 + (pk ? fc * 2 + t : perm8(fc * 2 + t));
-        if (n >= p.N || (pk && fc >= 2)) continue;
+        if (n >= nend || (pk && fc >= 2)) continue;
         // explicit roundings (no contraction choices left to the compiler): every
         // instantiation -- tile shape, sum planes or not -- rounds the same way, so a
         // product is bit-identical whichever config the planner picks without split-K
