@@ -396,16 +396,20 @@ Plan choose_sums_rule(long long M, long long N, long long K) {
   // 24-column tiles of the row-stacked 32-wide kernel (cfg 15: every warp spans the tile's
   // columns, so a 24-column tile keeps 3 live blocks in every warp) in one launch --
   // no ragged last tile, whose loads cost >= 0.86 of a full tile whatever it holds.
-  if (!bonly && mixed_tiles()) {
+  // Measured at n = 20000 (profiles/r02/mixed_tiles.json): k = 80 +6.1 %, 100-104 +5 %,
+  // 200 +3.5 %; equal within 0.3 % where the plain plans pad little (201-232, 400); worse
+  // on wide blocks (1100: -6.7 %, 2200: -9.3 %) and at 136 (-1.4 %). So it is taken only
+  // up to 512 columns and when the best plain plan pads >= 7 % more columns.
+  if (!bonly && mixed_tiles() && N <= 512) {
     const long long m8 = (N + 7) / 8;
+    const long long pad_plain =
+        ((N + kBN[best.cfg] - 1) / kBN[best.cfg]) * (long long)kBN[best.cfg];
     for (long long b = 1; b <= 3; ++b) {
       const long long rest = m8 - 3 * b;
       if (rest < 0 || rest % 4 != 0) continue;
       const long long a = rest / 4;
       if (a < 1) break;  // 24-column tiles only: cfg 16 is that plan
-      const double score = (double)(8 * m8) * 1.004 * (1.0 + 0.02 * (double)b / (double)(a + b));
-      if (score < best_score) {
-        best_score = score;
+      if ((double)pad_plain >= 1.07 * (double)(8 * m8)) {
         best.cfg = FIRST_SUMS + 1;
         best.n_wide = (int)a;
         best.n_narrow = (int)b;
