@@ -666,7 +666,7 @@ def reference_window_leg(H, lam, rank, world, dev, nev=2000, nex=200, degree=25,
         if (n, nev, nex, degree) == (20000, 2000, 200, 25):
             out["est_s_per_solve"] = wide * t_head + narrow * t_tail
             out["est_basis"] = (f"one-GPU reference-interval trace: {wide} full-width + "
-                                f"{narrow} narrow iterations (measured 1-GPU solve 2007 s)")
+                                f"{narrow} narrow iterations (measured 1-GPU solve 2012 s)")
     except Exception:  # pragma: no cover - informational
         pass
     return out
