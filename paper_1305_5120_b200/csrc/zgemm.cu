@@ -358,7 +358,7 @@ bool mixed_tiles() {
   }();
   return on;
 }
-bool narrow_inloop(long long N) {
+bool narrow_bsums(long long N) {
   static const bool on = [] {
     const char* e = getenv("CHFSI_NARROW_INLOOP");
     return !(e && atoi(e) == 0);
@@ -371,7 +371,7 @@ Plan choose_sums_rule(long long M, long long N, long long K) {
   double best_score = 1e300;
   const long long tm = (M + 63) / 64;
   // the kernel family: both sum planes, or (narrow blocks) the B-sum plane only
-  const bool bonly = narrow_inloop(N);
+  const bool bonly = narrow_bsums(N);
   const int c_lo = bonly ? FIRST_BSUMS : FIRST_SUMS, c_hi = bonly ? NCFG : FIRST_BSUMS;
   for (int c = c_lo; c < c_hi; ++c) {
     const long long tn = (N + kBN[c] - 1) / kBN[c];
