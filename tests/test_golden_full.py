@@ -100,3 +100,33 @@ def test_c2_problem1_generalized_matches_reference():
     n_ref = len(g["it_filtered"])
     assert abs(rep.reports[0].outer_iterations - n_ref) <= max(2, 0.02 * n_ref), \
         (rep.reports[0].outer_iterations, n_ref)
+
+
+def test_generalized_reuse_sequence_matches_reference():
+    """A 3-problem generalized reuse sequence at c1 size (n = 2000, one S, nev = 200,
+    nex = 40, m = 20; tests/golden/g2000_sequence.npz, scripts/make_golden.py --g2000)
+    against the reference's own solve_sequence run: problems 2 and 3 -- warm starts
+    mapped through L^H, inherited interval estimates -- match in eigenvalues, subspace,
+    B-orthonormality, generalized residual and outer-iteration count (+-2 %)."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    g = _load("g2000_sequence.npz")
+    probs = baseline_sequence(5, 2000, 3, generalized=True)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=2000, N=3, nev=200, seed=0,
+                                                kind="generalized"),
+                            problems=list(probs))
+    cfg = G.SolverConfig(nev=200, buffer=40, degree=20, max_outer_iters=20000)
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
+    seed = int(g["probe_seed"])
+    for i, (a, s) in enumerate(probs):
+        lam, c = rep.eigenvalues[i], rep.vectors[i].entries
+        lam_ref = g[f"lam{i}"]
+        assert len(lam) == len(lam_ref) == 200
+        assert np.max(np.abs(lam - lam_ref) / np.abs(lam_ref)) <= 1e-10, i
+        assert np.linalg.norm(c.conj().T @ s @ c - np.eye(200)) <= 1e-9, i
+        res = np.linalg.norm(a @ c - (s @ c) * lam, axis=0)
+        assert np.max(res) <= cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(s, 1)), i
+        assert _sketch_angle(c, g[f"sketch{i}"], seed) < 1e-8, i
+        n_ref = len(g[f"it_filtered{i}"])
+        assert abs(rep.reports[i].outer_iterations - n_ref) <= max(2, 0.02 * n_ref), \
+            (i, rep.reports[i].outer_iterations, n_ref)
