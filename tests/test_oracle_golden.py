@@ -155,3 +155,24 @@ def test_c1_full_fixture_trace_prefix():
     assert [r["filtered_cols"] for r in rep["iterations"]] == g["it_filtered0"][:25].tolist()
     mr = np.array([r["max_resid"] for r in rep["iterations"]])
     assert np.max(np.abs(mr - g["it_max_resid0"][:25]) / g["it_max_resid0"][:25]) <= 1e-6
+
+
+def test_generalized_sequence_fixture_trace_prefix():
+    """The generalized reuse sequence fixture (n = 2000, the reference's own
+    solve_sequence run, tests/golden/g2000_sequence.npz), problem 1: the oracle's
+    solve_generalized, seeded like the reference's sequence driver, retraces the first 20
+    outer iterations -- filtered columns, converged counts and residual maxima."""
+    import os
+    path = os.path.join(GOLD, "g2000_sequence.npz")
+    if not os.path.exists(path):
+        pytest.skip("g2000_sequence.npz not generated")
+    g = np.load(path)
+    a, s = baseline_sequence(5, 2000, 1, generalized=True)[0]
+    with pytest.raises(O.OracleError) as exc:
+        O.solve_generalized(a, s, None, 200, 40, 20, 1e-10, 20,
+                            seed=np.random.default_rng([0, 11, 1]))
+    rep = exc.value.info["report"]
+    assert [r["filtered_cols"] for r in rep["iterations"]] == g["it_filtered0"][:20].tolist()
+    assert [r["converged"] for r in rep["iterations"]] == g["it_converged0"][:20].tolist()
+    mr = np.array([r["max_resid"] for r in rep["iterations"]])
+    assert np.max(np.abs(mr - g["it_max_resid0"][:20]) / g["it_max_resid0"][:20]) <= 1e-6
