@@ -1,7 +1,7 @@
 """ncu driver: filter calls (chfsi_filter, 3M sum planes when on) at one shape with H
 declared, as inside a solve.
 
-    python scripts/profile_filter_call.py [n] [k] [degree]
+    python scripts/profile_filter_call.py [n] [k] [degree] [forced cfg] [forced split]
 """
 import sys
 
@@ -13,6 +13,10 @@ from paper_1305_5120_b200 import device as D  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 k = int(sys.argv[2]) if len(sys.argv) > 2 else 2200
 deg = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+if len(sys.argv) > 4:
+    from paper_1305_5120_b200 import _native  # noqa: E402
+    assert _native.load().chfsi_gemm_override(int(sys.argv[4]),
+                                              int(sys.argv[5]) if len(sys.argv) > 5 else 0) == 0
 dev = torch.device("cuda", 0)
 eng = D.Engine.get(dev)
 g = torch.Generator(device=dev)
