@@ -10,6 +10,9 @@ reference /root/reference/pkg/src/chfsi in the build container):
   nev = 200, nex = 40, m = 20, tol 1e-10 (about 20 min of CPU on 8 cores).
 * tests/golden/c2p1_full.npz -- BASELINE config 2, problem 1: generalized n = 5000,
   nev = 500, nex = 50, m = 20 (reference solve_generalized via solve_sequence).
+* tests/golden/c2p12_full.npz -- the same sequence's problems 1 AND 2 in reuse mode
+  (--c2p12, 4120 s of CPU), and tests/golden/g2000_sequence.npz -- a 3-problem
+  generalized reuse sequence at n = 2000 (--g2000).
 
 The n x nev eigenvector blocks are not stored; a subspace sketch is: P Z with P the
 orthogonal projector onto span(V) and Z a seeded n x 8 complex Gaussian probe.
@@ -124,6 +127,35 @@ def test_generalized_reuse_sequence_matches_reference():
         assert len(lam) == len(lam_ref) == 200
         assert np.max(np.abs(lam - lam_ref) / np.abs(lam_ref)) <= 1e-10, i
         assert np.linalg.norm(c.conj().T @ s @ c - np.eye(200)) <= 1e-9, i
+        res = np.linalg.norm(a @ c - (s @ c) * lam, axis=0)
+        assert np.max(res) <= cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(s, 1)), i
+        assert _sketch_angle(c, g[f"sketch{i}"], seed) < 1e-8, i
+        n_ref = len(g[f"it_filtered{i}"])
+        assert abs(rep.reports[i].outer_iterations - n_ref) <= max(2, 0.02 * n_ref), \
+            (i, rep.reports[i].outer_iterations, n_ref)
+
+
+def test_c2_problems_1_and_2_generalized_reuse_match_reference():
+    """BASELINE c2 problems 1 and 2 (generalized, n = 5000, nev = 500) through
+    solve_sequence in reuse mode against the reference's own run of the same two cycles
+    (tests/golden/c2p12_full.npz, scripts/make_golden.py --c2p12): problem 2 starts from
+    problem 1's eigenvectors (mapped through L^H) with the inherited interval estimates."""
+    import paper_1305_5120_b200 as G
+    from paper_1305_5120_b200.workloads import baseline_sequence
+    g = _load("c2p12_full.npz")
+    probs = baseline_sequence(0, 5000, 2, generalized=True)
+    seq = G.ProblemSequence(spec=G.SequenceSpec(n=5000, N=2, nev=500, seed=0,
+                                                kind="generalized"),
+                            problems=list(probs))
+    cfg = G.SolverConfig(nev=500, buffer=50, degree=20, max_outer_iters=20000)
+    rep = G.solve_sequence(seq, cfg, "reuse", angles=False)
+    seed = int(g["probe_seed"])
+    for i, (a, s) in enumerate(probs):
+        lam, c = rep.eigenvalues[i], rep.vectors[i].entries
+        lam_ref = g[f"lam{i}"]
+        assert len(lam) == len(lam_ref) == 500
+        assert np.max(np.abs(lam - lam_ref) / np.abs(lam_ref)) <= 1e-10, i
+        assert np.linalg.norm(c.conj().T @ s @ c - np.eye(500)) <= 1e-9, i
         res = np.linalg.norm(a @ c - (s @ c) * lam, axis=0)
         assert np.max(res) <= cfg.tol * (np.linalg.norm(a, 1) + np.linalg.norm(s, 1)), i
         assert _sketch_angle(c, g[f"sketch{i}"], seed) < 1e-8, i
